@@ -1,0 +1,201 @@
+/*
+ * s2v.h -- C ABI of libs2v.so, the sm_100a implementation of the
+ * OpenGraphGym-MG structure2vec-DQN hot path (arXiv 2105.08764).
+ *
+ * Every entry point takes plain pointers (device pointers unless stated) and
+ * sizes plus a cudaStream_t passed as void*; no torch types cross the boundary.
+ * The host mirror of the reference's Python API (paper_2105_08764_b200/) binds
+ * these with ctypes, exactly as a maintainer would bind them from the
+ * reference's own `graphrl` package (INTEGRATION.md shows the stub).
+ *
+ * Each function cites the reference interface it replaces (paths relative to
+ * /root/reference).  All calls are asynchronous on `stream` unless noted and
+ * return an s2v_status; s2v_last_error() returns the message of the last
+ * failure on the calling thread.
+ *
+ * Data layout:
+ *   - a batch of B graphs with the same node count N, row-partitioned over P
+ *     ranks (balanced blocks, pkg/src/graphrl/state.py:36-53);
+ *   - embedding buffers are node-major [B][P][rows_max][K]; the physical row of
+ *     node u of slot b owned by rank r is phys = (b*P + r)*rows_max + (u - row_start_r);
+ *   - a local residual CSR over this rank's B*num_rows rows whose column entries
+ *     hold the neighbour's physical row, ascending in original node id, with
+ *     bit 31 set once the edge is removed (the reference zeroes the value,
+ *     pkg/src/graphrl/state.py:173-208).
+ */
+#ifndef S2V_H_
+#define S2V_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  S2V_OK = 0,
+  S2V_EINVAL = 1,      /* ValueError                                   */
+  S2V_EACTION = 2,     /* InvalidActionError (state.py:181-194)        */
+  S2V_ECOMM = 3,       /* CollectiveError (collective.py:72-76)        */
+  S2V_ECUDA = 4,       /* CUDA runtime failure                         */
+  S2V_ENONFINITE = 5   /* non-finite gradient / target (policy.py:346) */
+} s2v_status;
+
+typedef enum { S2V_F32 = 0, S2V_F64 = 1 } s2v_dtype;
+
+#define S2V_DEAD 0x80000000u
+
+/* Residual graph shard of one rank (all pointers are device pointers).
+ * Replaces PartitionedState's scipy CSR + sol/cand/local_residual
+ * (pkg/src/graphrl/state.py:56-111). */
+typedef struct {
+  int64_t num_nodes;       /* N                                             */
+  int32_t batch;           /* B                                             */
+  int32_t world;           /* P                                             */
+  int32_t rank;            /* r                                             */
+  int32_t _pad;
+  int64_t row_start;       /* first global node owned by this rank          */
+  int64_t num_rows;        /* rows owned by this rank (per slot)            */
+  int64_t rows_max;        /* padded rows per rank in embedding buffers     */
+  int64_t nnz;             /* local entries over all slots                  */
+  const int64_t *row_ptr;  /* [B*num_rows+1]                                */
+  uint32_t *cols;          /* [nnz] phys neighbour row | S2V_DEAD           */
+  const int64_t *col_ptr;  /* [B*N+1] local entries whose column is (b,u)   */
+  const int64_t *col_ent;  /* [nnz]  entry index of those entries           */
+  const int32_t *col_row;  /* [nnz]  local row (b*num_rows+i) of the entry  */
+  int32_t *rdeg;           /* [B*num_rows] residual degree                  */
+  uint8_t *sol;            /* [B*num_rows] partial solution S               */
+  uint8_t *cand;           /* [B*num_rows] candidate set C                  */
+  int64_t *residual;       /* [B] alive local entries                       */
+} s2v_shard;
+
+/* ---- library ------------------------------------------------------------ */
+const char *s2v_last_error(void);
+const char *s2v_version(void);
+/* Set the device of the calling thread (one thread/process per GPU). */
+int s2v_set_device(int device);
+
+/* ---- state (pkg/src/graphrl/state.py) ----------------------------------- */
+/* Mark dead entries, compute rdeg/sol/cand/residual from a solution vector
+ * indexed by physical row (sol_phys[B*P*rows_max]).  Replaces the residual
+ * mask + row sums of PartitionedState.__init__ (state.py:89-111). */
+int s2v_shard_init(const s2v_shard *sh, const uint8_t *sol_phys, void *stream);
+
+/* Apply one group of picks per slot (picks[B*d], -1 padded, global node ids)
+ * with the reference's mid-group skip rule.  Replaces the group loop of
+ * inference._solve_batch (inference.py:125-146) and apply_action
+ * (state.py:173-208).  Two phases so that P>1 can exchange `info` between them:
+ *   phase 1 (owner side): info[B*d*2] int64 = {rdeg(v_j), alive-adjacency mask
+ *            of v_j to v_0..v_{d-1}} for locally owned picks, 0 elsewhere;
+ *   (P>1: sum-all-reduce info over ranks)
+ *   phase 2 (every rank): replay the skip rule, apply accepted picks to local
+ *            rows/columns, write applied[B*d] (uint8) and removed[B] (int64,
+ *            global entries removed = 2 * rdeg at apply time).
+ * `validate` = 1 checks pick 0 of every slot is a candidate (owner side) and
+ * fails with S2V_EACTION otherwise. */
+int s2v_apply_phase1(const s2v_shard *sh, const int64_t *picks, int d, int64_t *info,
+                     int validate, int32_t *err_out, void *stream);
+int s2v_apply_phase2(const s2v_shard *sh, const int64_t *picks, int d, const int64_t *info,
+                     uint8_t *applied, int64_t *removed, void *stream);
+
+/* ---- policy forward (pkg/src/graphrl/policy.py:144-224) ------------------ */
+/* e12 table: table[(deg)][K] for deg in [0,max_deg] (sol=0) and row max_deg+1
+ * for sol=1 (deg 0): fl(theta1*sol + fmachain(theta3, relu(theta2*deg))).
+ * Replaces policy.py:157-161. */
+int s2v_e12_table(s2v_dtype dt, const void *theta1, const void *theta2, const void *theta3,
+                  int K, int max_deg, void *table, void *stream);
+
+/* One embedding round over this rank's rows.  h_in == NULL means h = 0 (round
+ * 1).  Writes h_out at this rank's physical rows; optionally m_out (the
+ * aggregated neighbour sums, [B*num_rows][K]) for the training tape.
+ * Replaces one iteration of policy.py:163-174 (spmm state.py:157-162 +
+ * embed_fwd all-reduce + theta4 projection + relu). */
+int s2v_embed_round(s2v_dtype dt, const s2v_shard *sh, const void *theta4, const void *table,
+                    int K, int max_deg, const void *h_in, void *h_out, void *m_out,
+                    void *stream);
+
+/* g[b][k] = numpy pairwise sum over the N nodes of slot b of h[.,k]; h must
+ * hold every rank's rows (after an all-gather when P>1).  Replaces
+ * embed.sum(axis=2) + q_fwd all-reduce (policy.py:199-200). */
+int s2v_colsum(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, void *g,
+               void *workspace, size_t workspace_bytes, void *stream);
+size_t s2v_colsum_workspace(const s2v_shard *sh, int K, int elem_bytes);
+
+/* Scores of this rank's rows: u2 = theta6 (h*cand), r = relu([u1;u2]),
+ * score = sum_j fl(r_j theta7_j) (policy.py:201-207), masked selection keys
+ * (policy.py:221-224 + inference.py:61-73 / agent.py:169) and per-block
+ * top-8 keys.  cand_override (nullable, [B*num_rows]) replaces sh->cand as
+ * the extractor (q_forward's `cand` argument).  mode 0 = solve semantics
+ * (candidates with finite score), mode 1 = argmax/max semantics (NaN wins).
+ * Outputs: scores[B*num_rows]; block_keys[B][nblk][8]; counts[B] (int64,
+ * number of selectable nodes). */
+int s2v_score(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, const void *u1,
+              const void *theta6, const void *theta7, const uint8_t *cand_override,
+              int mode, void *scores, uint64_t *block_keys, int64_t *counts, void *stream);
+int s2v_score_blocks(const s2v_shard *sh);
+/* Merge per-block keys into the top-d (d <= 8) keys per slot, descending.
+ * A key is two uint64 {orderable(score), ~node}; {0,0} = none. */
+int s2v_topk_merge(const s2v_shard *sh, const uint64_t *block_keys, int d, uint64_t *top,
+                   void *stream);
+
+/* ---- policy backward + Adam (policy.py:232-359) -------------------------- */
+/* Number of CTAs (= partial rows) used by the backward reductions. */
+int s2v_backward_blocks(const s2v_shard *sh);
+/* grad_h[r] = dg[b] (+ dact[b] at the action row of slot b): the adjoint of
+ * g = sum(embed) broadcast to every node plus the head term (policy.py:282-288). */
+int s2v_grad_h_init(s2v_dtype dt, const s2v_shard *sh, int K, const void *dg,
+                    const int64_t *actions, const void *dact, void *grad_h, void *stream);
+/* One layer of policy.py:290-303: dz = grad_h * (h_l > 0); dzsum (+)= dz;
+ * partial[blk][K*K] (+)= dz (x) m_l (m_l NULL for layer 1); dm = theta4^T dz
+ * written at this rank's physical rows of dm_out (NULL for layer 1).
+ * first = 1 initialises dzsum and partial instead of accumulating. */
+int s2v_layer_backward(s2v_dtype dt, const s2v_shard *sh, int K, const void *theta4,
+                       const void *grad_h, const void *h_l, const void *m_l, void *dzsum,
+                       void *partial, int first, void *dm_out, void *stream);
+/* out[r] = sum over alive neighbours (ascending id) of src[phys] -- spmm_t
+ * (state.py:164-169); src holds every rank's rows. */
+int s2v_gather(s2v_dtype dt, const s2v_shard *sh, int K, const void *src, void *out,
+               void *stream);
+/* Partials [blk][2K + K*K] of dtheta1, dtheta2, dtheta3 from dzsum
+ * (policy.py:294-296,305-306; dw_acc = theta3^T dzsum by linearity). */
+int s2v_param_grads(s2v_dtype dt, const s2v_shard *sh, int K, const void *theta2,
+                    const void *theta3, const void *dzsum, void *partials, void *stream);
+/* out[len] (fp64) = sum over nparts partial rows, fixed order. */
+int s2v_reduce_partials(s2v_dtype dt, const void *partials, int nparts, int len, double *out,
+                        void *stream);
+/* Q head at the action node of every slot owned by this rank
+ * (policy.py:256-283): head_out[b][2K*K + 2K + 1] fp64 = dtheta5, dtheta6,
+ * dtheta7, squared error; dg[b][K] = theta5^T dpre[:K]; dact[b][K] =
+ * theta6^T dpre[K:].  Zeros for slots whose action another rank owns. */
+int s2v_head_backward(s2v_dtype dt, const s2v_shard *sh, int K, const void *h_L,
+                      const void *g, const int64_t *actions, const void *targets,
+                      const void *theta5, const void *theta6, const void *theta7,
+                      double *head_out, void *dg, void *dact, void *stream);
+/* Bias-corrected Adam with the reference's element-wise rounding
+ * (policy.py:339-359); omb1/omb2 = the host's (1 - beta1), (1 - beta2);
+ * b1c/b2c = 1 - beta^t computed on the host in fp64. */
+int s2v_adam(s2v_dtype dt, void *params, const void *grads, void *m, void *v, int64_t n,
+             double beta1, double omb1, double beta2, double omb2, double eps, double lr,
+             double b1c, double b2c, void *stream);
+
+/* ---- graph ingestion (graphs.py:125-157) --------------------------------- */
+/* Bit-exact generate_ba from numpy's PCG64 state {state_hi, state_lo, inc_hi,
+ * inc_lo, has_uint32, uinteger} (host memory).  edges_out == NULL returns E. */
+int64_t s2v_generate_ba(int64_t n, int64_t d, const void *pcg, void *edges_out);
+
+/* ---- collectives (replaces collective.py's in-process Comm) -------------- */
+int s2v_comm_unique_id(void *out, size_t len);
+int s2v_comm_init(const void *unique_id, int world, int rank, void **comm);
+int s2v_comm_destroy(void *comm);
+/* in-place when send == recv + rank*bytes */
+int s2v_comm_allgather(void *comm, const void *send, void *recv, size_t bytes, void *stream);
+int s2v_comm_allgather_slots(void *comm, void *recv, size_t bytes, size_t slot_stride,
+                             int nslots, int rank, void *stream);
+int s2v_comm_allreduce(void *comm, void *buf, size_t count, int kind /*0 i64 1 f64 2 f32*/,
+                       void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* S2V_H_ */

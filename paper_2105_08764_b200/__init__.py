@@ -1,0 +1,17 @@
+"""paper_2105_08764_b200 -- B200-native (sm_100a) hot path of OpenGraphGym-MG.
+
+Drop-in for the reference `graphrl` package's parallel RL inference/training
+step: the same public names and signatures, with the numerics in libs2v.so
+(hand-written CUDA for sm_100a behind a C ABI, include/s2v.h) and the node
+shards resident in HBM.  There is no CPU compute path.
+"""
+from .collective import Comm, CollectiveStats, DistComm, WorkerGroup, run_workers
+from .errors import (CollectiveAborted, CollectiveError, ConfigError, DataError, GraphRLError,
+                     InvalidActionError)
+from .graphs import Graph, generate_ba, generate_er, generate_rmat, load_edge_list, write_edge_list
+from .inference import SelectionSchedule, SolveResult, select_top_d, solve
+from .policy import (PolicyParams, embed_forward, load_checkpoint, masked_scores, q_forward,
+                     save_checkpoint)
+from .state import Partition, PartitionedState, apply_action, is_covered, partition_rows
+
+__version__ = "0.1.0"

@@ -1,0 +1,129 @@
+"""ctypes binding of libs2v.so (include/s2v.h) -- the only compute path.
+
+There is no CPU fallback: importing a compute entry point without the built
+extension, or without a CUDA device, raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import CollectiveError, InvalidActionError
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = PKG_DIR / "libs2v.so"
+
+S2V_OK, S2V_EINVAL, S2V_EACTION, S2V_ECOMM, S2V_ECUDA, S2V_ENONFINITE = range(6)
+S2V_F32, S2V_F64 = 0, 1
+KEY_BYTES = 16  # struct Key {uint64 s; uint64 inv;}
+TOPK_MAX = 8
+
+
+class s2v_shard(ctypes.Structure):
+    _fields_ = [
+        ("num_nodes", ctypes.c_int64),
+        ("batch", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+        ("row_start", ctypes.c_int64),
+        ("num_rows", ctypes.c_int64),
+        ("rows_max", ctypes.c_int64),
+        ("nnz", ctypes.c_int64),
+        ("row_ptr", ctypes.c_void_p),
+        ("cols", ctypes.c_void_p),
+        ("col_ptr", ctypes.c_void_p),
+        ("col_ent", ctypes.c_void_p),
+        ("col_row", ctypes.c_void_p),
+        ("rdeg", ctypes.c_void_p),
+        ("sol", ctypes.c_void_p),
+        ("cand", ctypes.c_void_p),
+        ("residual", ctypes.c_void_p),
+    ]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_SZ = ctypes.c_size_t
+_D = ctypes.c_double
+_SH = ctypes.POINTER(s2v_shard)
+
+_SIGNATURES = {
+    "s2v_last_error": ([], ctypes.c_char_p),
+    "s2v_version": ([], ctypes.c_char_p),
+    "s2v_set_device": ([_I], _I),
+    "s2v_shard_init": ([_SH, _P, _P], _I),
+    "s2v_apply_phase1": ([_SH, _P, _I, _P, _I, _P, _P], _I),
+    "s2v_apply_phase2": ([_SH, _P, _I, _P, _P, _P, _P], _I),
+    "s2v_e12_table": ([_I, _P, _P, _P, _I, _I, _P, _P], _I),
+    "s2v_embed_round": ([_I, _SH, _P, _P, _I, _I, _P, _P, _P, _P], _I),
+    "s2v_colsum": ([_I, _SH, _I, _P, _P, _P, _SZ, _P], _I),
+    "s2v_colsum_workspace": ([_SH, _I, _I], _SZ),
+    "s2v_score": ([_I, _SH, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P], _I),
+    "s2v_score_blocks": ([_SH], _I),
+    "s2v_topk_merge": ([_SH, _P, _I, _P, _P], _I),
+    "s2v_backward_blocks": ([_SH], _I),
+    "s2v_grad_h_init": ([_I, _SH, _I, _P, _P, _P, _P, _P], _I),
+    "s2v_layer_backward": ([_I, _SH, _I, _P, _P, _P, _P, _P, _P, _I, _P, _P], _I),
+    "s2v_gather": ([_I, _SH, _I, _P, _P, _P], _I),
+    "s2v_param_grads": ([_I, _SH, _I, _P, _P, _P, _P, _P], _I),
+    "s2v_reduce_partials": ([_I, _P, _I, _I, _P, _P], _I),
+    "s2v_head_backward": ([_I, _SH, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I),
+    "s2v_adam": ([_I, _P, _P, _P, _P, _I64, _D, _D, _D, _D, _D, _D, _D, _D, _P], _I),
+    "s2v_comm_unique_id": ([_P, _SZ], _I),
+    "s2v_comm_init": ([_P, _I, _I, ctypes.POINTER(ctypes.c_void_p)], _I),
+    "s2v_comm_destroy": ([_P], _I),
+    "s2v_comm_allgather": ([_P, _P, _P, _SZ, _P], _I),
+    "s2v_comm_allgather_slots": ([_P, _P, _SZ, _SZ, _I, _I, _P], _I),
+    "s2v_comm_allreduce": ([_P, _P, _SZ, _I, _P], _I),
+    "s2v_generate_ba": ([_I64, _I64, _P, _P], _I64),
+}
+
+_lib = None
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGNATURES)
+
+
+def load() -> ctypes.CDLL:
+    """Load libs2v.so (built by __graft_entry__.build()); fail loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build the CUDA extension first "
+            "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    import torch  # noqa: F401  -- loads the CUDA runtime / NCCL torch was built with
+    lib = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_GLOBAL if hasattr(os, "RTLD_GLOBAL") else 0)
+    missing = [n for n in _SIGNATURES if not hasattr(lib, n)]
+    if missing:
+        raise RuntimeError(f"{LIB_PATH} is stale: missing symbols {missing}; rebuild it")
+    for name, (args, res) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map an s2v_status onto the reference's exception types."""
+    if rc == S2V_OK:
+        return
+    msg = load().s2v_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == S2V_EACTION:
+        raise InvalidActionError(text)
+    if rc == S2V_ECOMM:
+        raise CollectiveError(text)
+    if rc in (S2V_EINVAL, S2V_ENONFINITE):
+        raise ValueError(text)
+    raise RuntimeError(f"libs2v CUDA failure: {text}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

@@ -1,0 +1,304 @@
+"""Worker groups: host rendezvous collectives + NCCL device collectives.
+
+API mirrors pkg/src/graphrl/collective.py (WorkerGroup, Comm, run_workers,
+CollectiveStats).  Two kinds of traffic:
+
+* host collectives on small numpy arrays (candidacy flags, targets, counts):
+  rank-ordered, by value, exactly the reference semantics -- through an
+  in-process rendezvous when ranks are threads (run_workers), or through
+  torch.distributed (gloo) when ranks are processes (torchrun, DistComm);
+* device collectives on HBM buffers (per-round halo all-gather of embeddings,
+  selection info, gradient packs): NCCL over NVLink, owned by libs2v
+  (s2v_comm_*), one communicator per rank, created lazily.
+
+Each rank binds one CUDA device: rank r of a thread group uses device
+r % device_count, a torchrun process uses LOCAL_RANK.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import CollectiveAborted, CollectiveError
+
+DEFAULT_TIMEOUT = 30.0
+
+
+@dataclass
+class CollectiveStats:
+    """Per-tag instrumentation: logical calls and per-rank elements sent."""
+    calls: int = 0
+    elements: int = 0
+
+
+class WorkerGroup:
+    """A fixed set of P cooperating thread-ranks and their rendezvous."""
+
+    def __init__(self, num_workers: int, timeout: float = DEFAULT_TIMEOUT):
+        if num_workers < 1:
+            raise ValueError(f"num_workers must be >= 1, got {num_workers}")
+        self.num_workers = int(num_workers)
+        self.timeout = float(timeout)
+        self._slots: list = [None] * self.num_workers
+        self._barrier = threading.Barrier(self.num_workers)
+        self._stats: dict[str, CollectiveStats] = {}
+        self._lock = threading.Lock()
+        self._nccl_id: bytes | None = None
+
+    def comm(self, rank: int) -> "Comm":
+        if not 0 <= rank < self.num_workers:
+            raise ValueError(f"rank {rank} out of range for P={self.num_workers}")
+        return Comm(self, rank)
+
+    def abort(self) -> None:
+        self._barrier.abort()
+
+    def stats_snapshot(self) -> dict[str, CollectiveStats]:
+        with self._lock:
+            return {t: CollectiveStats(s.calls, s.elements) for t, s in self._stats.items()}
+
+    def reset_stats(self) -> None:
+        with self._lock:
+            self._stats.clear()
+
+    def _record(self, tag: str, elements: int) -> None:
+        with self._lock:
+            st = self._stats.setdefault(tag, CollectiveStats())
+            st.calls += 1
+            st.elements += int(elements)
+
+    def _wait(self) -> None:
+        try:
+            self._barrier.wait(timeout=self.timeout)
+        except threading.BrokenBarrierError:
+            raise CollectiveAborted(
+                f"collective aborted: a rank failed or did not arrive within "
+                f"{self.timeout:.1f}s (P={self.num_workers})") from None
+
+    def _exchange(self, rank: int, value) -> list:
+        # deposit a private copy, wait for everyone, snapshot, wait again so
+        # no rank overwrites its slot before all peers have read it
+        self._slots[rank] = np.array(value, copy=True)
+        self._wait()
+        out = list(self._slots)
+        self._wait()
+        return out
+
+
+class _DeviceComm:
+    """NCCL communicator of one rank (libs2v s2v_comm_*)."""
+
+    def __init__(self, unique_id: bytes, world: int, rank: int):
+        from . import _lib
+        self._lib = _lib
+        handle = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(unique_id, len(unique_id))
+        _lib.call("s2v_comm_init", buf, world, rank, ctypes.byref(handle))
+        self.handle = handle
+        self.world, self.rank = world, rank
+
+    def allgather_slots(self, buf_ptr: int, chunk_bytes: int, slot_stride: int, nslots: int,
+                        stream: int) -> None:
+        self._lib.call("s2v_comm_allgather_slots", self.handle, buf_ptr, chunk_bytes,
+                       slot_stride, nslots, self.rank, stream)
+
+    def allreduce(self, buf_ptr: int, count: int, kind: int, stream: int) -> None:
+        self._lib.call("s2v_comm_allreduce", self.handle, buf_ptr, count, kind, stream)
+
+    def close(self) -> None:
+        if self.handle:
+            self._lib.load().s2v_comm_destroy(self.handle)
+            self.handle = None
+
+
+def _new_unique_id() -> bytes:
+    from . import _lib
+    buf = ctypes.create_string_buffer(128)
+    _lib.call("s2v_comm_unique_id", buf, 128)
+    return buf.raw
+
+
+class Comm:
+    """Per-rank handle used to enter collectives (collective.py:92-146)."""
+
+    def __init__(self, group: WorkerGroup, rank: int):
+        self.group = group
+        self.rank = rank
+        self.size = group.num_workers
+        self._dev = None
+
+    # -- host collectives (reference semantics) -----------------------------
+
+    def all_reduce_sum(self, local, tag: str = "default") -> np.ndarray:
+        arr = np.asarray(local)
+        if self.rank == 0:
+            self.group._record(tag, arr.size)
+        slots = self.group._exchange(self.rank, arr)
+        shapes = [s.shape for s in slots]
+        if any(s != shapes[0] for s in shapes):
+            raise CollectiveError(f"all_reduce_sum shape mismatch across ranks: {shapes}")
+        out = slots[0].astype(np.result_type(*[s.dtype for s in slots]), copy=True)
+        for other in slots[1:]:
+            out += other
+        return out
+
+    def all_gather(self, local, axis: int = -1, tag: str = "default") -> np.ndarray:
+        arr = np.asarray(local)
+        if self.rank == 0:
+            self.group._record(tag, arr.size)
+        slots = self.group._exchange(self.rank, arr)
+        ref = list(slots[0].shape)
+        ax = axis % max(slots[0].ndim, 1) if slots[0].ndim else 0
+        for s in slots:
+            shp = list(s.shape)
+            if len(shp) != len(ref):
+                raise CollectiveError(f"all_gather rank mismatch: {[t.shape for t in slots]}")
+            if shp[:ax] != ref[:ax] or shp[ax + 1:] != ref[ax + 1:]:
+                raise CollectiveError(
+                    f"all_gather shape mismatch off the concat axis: {[t.shape for t in slots]}")
+        if self.size == 1:
+            return slots[0].copy()
+        return np.concatenate(slots, axis=axis)
+
+    def barrier(self) -> None:
+        self.group._wait()
+
+    # -- device collectives ------------------------------------------------
+
+    def record(self, tag: str, elements: int) -> None:
+        if self.rank == 0:
+            self.group._record(tag, elements)
+
+    def device_comm(self) -> _DeviceComm | None:
+        """Lazily create this rank's NCCL communicator (None when P == 1)."""
+        if self.size == 1:
+            return None
+        if self._dev is None:
+            uid = _new_unique_id() if self.rank == 0 else b""
+            ids = self.group._exchange(self.rank, np.frombuffer(uid or b"\0", dtype=np.uint8))
+            self._dev = _DeviceComm(bytes(ids[0]), self.size, self.rank)
+        return self._dev
+
+
+class DistComm:
+    """Comm over torch.distributed for one-process-per-GPU runs (torchrun).
+
+    Host collectives go through a gloo group (CPU numpy payloads); device
+    collectives through libs2v's own NCCL communicator.
+    """
+
+    def __init__(self):
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            raise RuntimeError("DistComm needs torch.distributed to be initialised")
+        self._dist = dist
+        self.rank = dist.get_rank()
+        self.size = dist.get_world_size()
+        self._gloo = dist.new_group(backend="gloo")
+        self._stats: dict[str, CollectiveStats] = {}
+        self.group = self
+        self._dev = None
+
+    def stats_snapshot(self):
+        return dict(self._stats)
+
+    def record(self, tag: str, elements: int) -> None:
+        if self.rank == 0:
+            st = self._stats.setdefault(tag, CollectiveStats())
+            st.calls += 1
+            st.elements += int(elements)
+
+    def _gather_objects(self, arr):
+        out = [None] * self.size
+        self._dist.all_gather_object(out, arr, group=self._gloo)
+        return out
+
+    def all_reduce_sum(self, local, tag: str = "default") -> np.ndarray:
+        arr = np.asarray(local)
+        self.record(tag, arr.size)
+        slots = self._gather_objects(arr)
+        out = slots[0].astype(np.result_type(*[s.dtype for s in slots]), copy=True)
+        for other in slots[1:]:
+            out += other
+        return out
+
+    def all_gather(self, local, axis: int = -1, tag: str = "default") -> np.ndarray:
+        arr = np.asarray(local)
+        self.record(tag, arr.size)
+        slots = self._gather_objects(arr)
+        return slots[0].copy() if self.size == 1 else np.concatenate(slots, axis=axis)
+
+    def barrier(self) -> None:
+        self._dist.barrier(group=self._gloo)
+
+    def device_comm(self):
+        if self.size == 1:
+            return None
+        if self._dev is None:
+            uid = [_new_unique_id() if self.rank == 0 else None]
+            self._dist.broadcast_object_list(uid, src=0, group=self._gloo)
+            self._dev = _DeviceComm(uid[0], self.size, self.rank)
+        return self._dev
+
+
+def run_workers(num_workers: int, fn, *args, timeout: float = DEFAULT_TIMEOUT,
+                group: WorkerGroup | None = None, bind_devices: bool = True) -> list:
+    """Run fn(comm, *args) on every rank (one thread per rank, each bound to
+    one CUDA device); results in rank order.  The first failure aborts the
+    group and is re-raised, root causes before knock-on aborts
+    (collective.py:149-195)."""
+    if group is None:
+        group = WorkerGroup(num_workers, timeout=timeout)
+    elif group.num_workers != num_workers:
+        raise ValueError("group size does not match num_workers")
+
+    def bind(rank: int) -> None:
+        if not bind_devices:
+            return
+        import torch
+        if torch.cuda.is_available():
+            from .device import bind_device
+            bind_device(rank % torch.cuda.device_count())
+
+    if num_workers == 1:
+        bind(0)
+        return [fn(group.comm(0), *args)]
+
+    results: list = [None] * num_workers
+    failures: list[tuple[int, BaseException]] = []
+    lock = threading.Lock()
+
+    def runner(rank: int) -> None:
+        try:
+            bind(rank)
+            results[rank] = fn(group.comm(rank), *args)
+        except BaseException as exc:  # noqa: BLE001 -- re-raised below
+            with lock:
+                failures.append((rank, exc))
+            group.abort()
+
+    threads = [threading.Thread(target=runner, args=(r,), name=f"s2v-rank-{r}")
+               for r in range(num_workers)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if failures:
+        def precedence(item):
+            exc = item[1]
+            if isinstance(exc, CollectiveAborted):
+                return 2
+            if isinstance(exc, CollectiveError):
+                return 1
+            return 0
+        failures.sort(key=lambda it: (precedence(it), it[0]))
+        raise failures[0][1]
+    return results
+
+
+def local_rank_from_env() -> int:
+    return int(os.environ.get("LOCAL_RANK", "0"))

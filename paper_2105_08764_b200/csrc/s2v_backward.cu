@@ -1,0 +1,456 @@
+// Hand-written DQN backward + Adam (sm_100a).
+//
+// Replaces (paths relative to /root/reference):
+//   loss_and_gradients   pkg/src/graphrl/policy.py:232-315
+//     head grads at the action nodes         policy.py:256-283
+//     dg all-reduce + broadcast              policy.py:285-288
+//     layer loop: dz, theta grads, dm, spmm_t policy.py:290-304, state.py:164-169
+//     theta2 grad                            policy.py:305-306
+//     fp64 gradient pack                     policy.py:308-314
+//   adam_step            pkg/src/graphrl/policy.py:339-359
+//
+// Parity bar for gradients/losses is 1e-4 relative, so the
+// K x K reductions use per-CTA partial sums in the parameter dtype and a
+// fixed-order fp64 reduction over CTAs: deterministic, hence bit-identical
+// replicas on every rank.  Adam follows the reference's element-wise fp32
+// rounding sequence exactly.
+#include "s2v_common.cuh"
+
+namespace s2v {
+
+constexpr int kBwdTile = 16;     // rows per tile
+constexpr int kBwdThreads = 256;
+
+inline int bwd_blocks(const s2v_shard &sh) {
+  int64_t rows = (int64_t)sh.batch * sh.num_rows;
+  int64_t tiles = (rows + kBwdTile - 1) / kBwdTile;
+  int64_t nb = tiles < kNumSMs * 2 ? tiles : kNumSMs * 2;
+  return (int)(nb < 1 ? 1 : nb);
+}
+
+__device__ __forceinline__ int64_t phys_of_row(const s2v_shard &sh, int64_t r) {
+  const int64_t b = r / sh.num_rows, i = r - b * sh.num_rows;
+  return (b * sh.world + sh.rank) * sh.rows_max + i;
+}
+
+// grad_h[r] = dg[b] (+ dact[b] at the action row of slot b)
+template <class T>
+__global__ void grad_h_init_kernel(s2v_shard sh, int K, const T *__restrict__ dg,
+                                   const int64_t *__restrict__ actions,
+                                   const T *__restrict__ dact, T *__restrict__ grad_h) {
+  const int64_t total = (int64_t)sh.batch * sh.num_rows * K;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / K;
+    const int k = (int)(idx - r * K);
+    const int64_t b = r / sh.num_rows, i = r - b * sh.num_rows;
+    T v = dg[b * K + k];
+    if (actions[b] == sh.row_start + i) v = addT(v, dact[b * K + k]);
+    grad_h[idx] = v;
+  }
+}
+
+// Layer backward over tiles of kBwdTile local rows.
+//   dz = grad_h * (h_l > 0); dzsum += dz; P4 += dz (x) m_l; dm = theta4^T dz
+template <class T>
+__global__ void __launch_bounds__(kBwdThreads) layer_backward_kernel(
+    s2v_shard sh, int K, const T *__restrict__ theta4, const T *__restrict__ grad_h,
+    const T *__restrict__ h_l, const T *__restrict__ m_l, T *__restrict__ dzsum,
+    T *__restrict__ partial, int first, T *__restrict__ dm_out) {
+  extern __shared__ unsigned char smem_raw[];
+  T *th = reinterpret_cast<T *>(smem_raw);  // [K][K+1] theta4
+  T *dz_s = th + K * (K + 1);               // [tile][K]
+  T *m_s = dz_s + kBwdTile * K;             // [tile][K]
+  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x)
+    th[(idx / K) * (K + 1) + (idx % K)] = theta4[idx];
+  const int KK = K * K;
+  const int per = (KK + blockDim.x - 1) / blockDim.x;  // outputs per thread (<= 64)
+  T acc[64];
+  for (int t = 0; t < per && t < 64; t++) {
+    int o = threadIdx.x + t * blockDim.x;
+    acc[t] = (!first && o < KK) ? partial[(int64_t)blockIdx.x * KK + o] : T(0);
+  }
+  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  const int64_t ntiles = (nrows + kBwdTile - 1) / kBwdTile;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kBwdTile;
+    __syncthreads();
+    for (int e = threadIdx.x; e < kBwdTile * K; e += blockDim.x) {
+      const int lr = e / K, k = e - lr * K;
+      const int64_t r = r0 + lr;
+      T dz = T(0), m = T(0);
+      if (r < nrows) {
+        const T hv = h_l[phys_of_row(sh, r) * K + k];
+        dz = (hv > T(0)) ? grad_h[r * K + k] : T(0);
+        dzsum[r * K + k] = first ? dz : addT(dzsum[r * K + k], dz);
+        if (m_l) m = m_l[r * K + k];
+      }
+      dz_s[e] = dz;
+      m_s[e] = m;
+    }
+    __syncthreads();
+    if (m_l) {
+      for (int t = 0; t < per && t < 64; t++) {
+        const int o = threadIdx.x + t * blockDim.x;
+        if (o >= KK) break;
+        const int k = o / K, j = o - k * K;
+        T a = acc[t];
+        for (int lr = 0; lr < kBwdTile; lr++) a = fmaT(dz_s[lr * K + k], m_s[lr * K + j], a);
+        acc[t] = a;
+      }
+    }
+    if (dm_out) {
+      for (int e = threadIdx.x; e < kBwdTile * K; e += blockDim.x) {
+        const int lr = e / K, j = e - lr * K;
+        const int64_t r = r0 + lr;
+        if (r >= nrows) continue;
+        T a = T(0);
+        for (int k = 0; k < K; k++) a = fmaT(th[k * (K + 1) + j], dz_s[lr * K + k], a);
+        dm_out[phys_of_row(sh, r) * K + j] = a;
+      }
+    }
+  }
+  for (int t = 0; t < per && t < 64; t++) {
+    int o = threadIdx.x + t * blockDim.x;
+    if (o < KK) partial[(int64_t)blockIdx.x * KK + o] = acc[t];
+  }
+}
+
+// out[r] = sum over alive neighbours (ascending) of src[phys]; one warp per row.
+template <class T>
+__global__ void gather_kernel(s2v_shard sh, int K, const T *__restrict__ src,
+                              T *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < nrows;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    for (int k0 = 0; k0 < K; k0 += 32) {
+      const int k = k0 + lane;
+      T a = T(0);
+      if (!sh.sol[r])
+        for (int64_t e = sh.row_ptr[r]; e < sh.row_ptr[r + 1]; e++) {
+          const uint32_t c = sh.cols[e];
+          if (c & S2V_DEAD) continue;
+          if (k < K) a = addT(a, src[(int64_t)c * K + k]);
+        }
+      if (k < K) out[r * K + k] = a;
+    }
+  }
+}
+
+// Partials of dtheta1 [K], dtheta2 [K], dtheta3 [K][K] from dzsum.
+template <class T>
+__global__ void __launch_bounds__(kBwdThreads) param_grads_kernel(
+    s2v_shard sh, int K, const T *__restrict__ theta2, const T *__restrict__ theta3,
+    const T *__restrict__ dzsum, T *__restrict__ partial) {
+  extern __shared__ unsigned char smem_raw[];
+  T *th3 = reinterpret_cast<T *>(smem_raw);  // [K][K+1]
+  T *dz_s = th3 + K * (K + 1);               // [tile][K]
+  T *w_s = dz_s + kBwdTile * K;              // [tile][K]
+  T *aux = w_s + kBwdTile * K;               // [tile][2]: sol, deg
+  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x)
+    th3[(idx / K) * (K + 1) + (idx % K)] = theta3[idx];
+  const int LEN = 2 * K + K * K;
+  const int per = (LEN + blockDim.x - 1) / blockDim.x;
+  T acc[72];
+  for (int t = 0; t < per && t < 72; t++) acc[t] = T(0);
+  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  const int64_t ntiles = (nrows + kBwdTile - 1) / kBwdTile;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kBwdTile;
+    __syncthreads();
+    for (int e = threadIdx.x; e < kBwdTile * K; e += blockDim.x) {
+      const int lr = e / K, k = e - lr * K;
+      const int64_t r = r0 + lr;
+      T dz = T(0), w = T(0);
+      if (r < nrows) {
+        dz = dzsum[r * K + k];
+        const T deg = sh.sol[r] ? T(0) : T(sh.rdeg[r]);
+        w = relu(mulT(theta2[k], deg));
+        if (k == 0) {
+          aux[2 * lr] = sh.sol[r] ? T(1) : T(0);
+          aux[2 * lr + 1] = deg;
+        }
+      } else if (k == 0) {
+        aux[2 * lr] = T(0);
+        aux[2 * lr + 1] = T(0);
+      }
+      dz_s[e] = dz;
+      w_s[e] = w;
+    }
+    __syncthreads();
+    for (int t = 0; t < per && t < 72; t++) {
+      const int o = threadIdx.x + t * blockDim.x;
+      if (o >= LEN) break;
+      T a = acc[t];
+      if (o < K) {  // dtheta1[k] = sum dz * sol
+        for (int lr = 0; lr < kBwdTile; lr++) a = fmaT(dz_s[lr * K + o], aux[2 * lr], a);
+      } else if (o < 2 * K) {  // dtheta2[j] = sum (theta3^T dz)_j * (w_j > 0) * deg
+        const int j = o - K;
+        for (int lr = 0; lr < kBwdTile; lr++) {
+          if (!(w_s[lr * K + j] > T(0))) continue;
+          T dw = T(0);
+          for (int k = 0; k < K; k++) dw = fmaT(th3[k * (K + 1) + j], dz_s[lr * K + k], dw);
+          a = fmaT(dw, aux[2 * lr + 1], a);
+        }
+      } else {  // dtheta3[k][j] = sum dz_k w_j
+        const int q = o - 2 * K, k = q / K, j = q - k * K;
+        for (int lr = 0; lr < kBwdTile; lr++) a = fmaT(dz_s[lr * K + k], w_s[lr * K + j], a);
+      }
+      acc[t] = a;
+    }
+  }
+  for (int t = 0; t < per && t < 72; t++) {
+    int o = threadIdx.x + t * blockDim.x;
+    if (o < LEN) partial[(int64_t)blockIdx.x * LEN + o] = acc[t];
+  }
+}
+
+template <class T>
+__global__ void reduce_partials_kernel(const T *__restrict__ partials, int nparts, int len,
+                                       double *__restrict__ out) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < len; o += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; p++) s += (double)partials[(int64_t)p * len + o];
+    out[o] = s;
+  }
+}
+
+// Q head at the action node of each slot (owner rank only).  head_out[b] =
+// [dtheta5 (K*K), dtheta6 (K*K), dtheta7 (2K), sq_err] in fp64.
+template <class T>
+__global__ void head_backward_kernel(s2v_shard sh, int K, const T *__restrict__ h_L,
+                                     const T *__restrict__ g, const int64_t *__restrict__ actions,
+                                     const T *__restrict__ targets, const T *__restrict__ t5,
+                                     const T *__restrict__ t6, const T *__restrict__ t7,
+                                     double *__restrict__ head_out, T *__restrict__ dg,
+                                     T *__restrict__ dact) {
+  extern __shared__ unsigned char smem_raw[];
+  T *hv = reinterpret_cast<T *>(smem_raw);  // [K]
+  T *gb = hv + K;                           // [K]
+  T *pre = gb + K;                          // [2K]
+  T *dpre = pre + 2 * K;                    // [2K]
+  __shared__ T s_delta;
+  __shared__ int s_owned;
+  const int b = blockIdx.x;
+  const int LEN = 2 * K * K + 2 * K + 1;
+  double *out = head_out + (int64_t)b * LEN;
+  const int64_t a = actions[b];
+  if (threadIdx.x == 0) s_owned = (a >= sh.row_start && a < sh.row_start + sh.num_rows);
+  __syncthreads();
+  if (!s_owned) {
+    for (int o = threadIdx.x; o < LEN; o += blockDim.x) out[o] = 0.0;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+      dg[(int64_t)b * K + k] = T(0);
+      dact[(int64_t)b * K + k] = T(0);
+    }
+    return;
+  }
+  const int64_t phys = ((int64_t)b * sh.world + sh.rank) * sh.rows_max + (a - sh.row_start);
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    hv[k] = h_L[phys * K + k];
+    gb[k] = g[(int64_t)b * K + k];
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 2 * K; k += blockDim.x) {
+    T acc = T(0);
+    if (k < K)
+      for (int p = 0; p < K; p++) acc = fmaT(t5[k * K + p], gb[p], acc);
+    else
+      for (int p = 0; p < K; p++) acc = fmaT(t6[(k - K) * K + p], hv[p], acc);
+    pre[k] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T q = T(0);
+    for (int j = 0; j < 2 * K; j++) q = addT(q, mulT(relu(pre[j]), t7[j]));
+    T err = q - targets[b];
+    out[LEN - 1] = (double)err * (double)err;
+    s_delta = (T(2) * err) / T(sh.batch);
+  }
+  __syncthreads();
+  const T delta = s_delta;
+  for (int j = threadIdx.x; j < 2 * K; j += blockDim.x) {
+    dpre[j] = pre[j] > T(0) ? mulT(delta, t7[j]) : T(0);
+    out[2 * K * K + j] = (double)mulT(delta, relu(pre[j]));
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < 2 * K * K; o += blockDim.x) {
+    if (o < K * K) {
+      const int k = o / K, p = o - k * K;
+      out[o] = (double)mulT(dpre[k], gb[p]);
+    } else {
+      const int q = o - K * K, k = q / K, p = q - k * K;
+      out[o] = (double)mulT(dpre[K + k], hv[p]);
+    }
+  }
+  for (int p = threadIdx.x; p < K; p += blockDim.x) {
+    T a5 = T(0), a6 = T(0);
+    for (int k = 0; k < K; k++) {
+      a5 = fmaT(t5[k * K + p], dpre[k], a5);
+      a6 = fmaT(t6[k * K + p], dpre[K + k], a6);
+    }
+    dg[(int64_t)b * K + p] = a5;
+    dact[(int64_t)b * K + p] = a6;
+  }
+}
+
+// Adam (policy.py:339-359) with numpy's NEP-50 rounding: every Python scalar
+// is cast to the array dtype, every op rounded separately.
+template <class T>
+__global__ void adam_kernel(T *__restrict__ p, const T *__restrict__ g, T *__restrict__ m,
+                            T *__restrict__ v, int64_t n, T b1, T omb1, T b2, T omb2, T eps,
+                            T lr, T b1c, T b2c) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T gi = g[i];
+    const T mi = addT(mulT(b1, m[i]), mulT(omb1, gi));
+    const T vi = addT(mulT(b2, v[i]), mulT(mulT(omb2, gi), gi));
+    m[i] = mi;
+    v[i] = vi;
+    const T mh = mi / b1c;
+    const T vh = vi / b2c;
+    const T upd = mulT(lr, mh) / addT(sqrt(vh), eps);
+    p[i] = p[i] - upd;
+  }
+}
+
+template <class T>
+static int layer_backward_t(const s2v_shard *sh, int K, const void *theta4, const void *grad_h,
+                            const void *h_l, const void *m_l, void *dzsum, void *partial,
+                            int first, void *dm_out, cudaStream_t st) {
+  if (K * K > 64 * kBwdThreads) return fail(S2V_EINVAL, "embed_dim %d too large for backward", K);
+  size_t smem = sizeof(T) * ((size_t)K * (K + 1) + 2 * kBwdTile * (size_t)K);
+  auto kern = layer_backward_kernel<T>;
+  S2V_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<bwd_blocks(*sh), kBwdThreads, smem, st>>>(*sh, K, (const T *)theta4, (const T *)grad_h,
+                                                   (const T *)h_l, (const T *)m_l, (T *)dzsum,
+                                                   (T *)partial, first, (T *)dm_out);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+}  // namespace s2v
+
+using namespace s2v;
+
+extern "C" {
+
+int s2v_backward_blocks(const s2v_shard *sh) { return bwd_blocks(*sh); }
+
+int s2v_grad_h_init(s2v_dtype dt, const s2v_shard *sh, int K, const void *dg,
+                    const int64_t *actions, const void *dact, void *grad_h, void *stream) {
+  int64_t total = (int64_t)sh->batch * sh->num_rows * K;
+  if (total == 0) return S2V_OK;
+  int grid = (int)std::min<int64_t>((total + 255) / 256, kNumSMs * 8);
+  if (dt == S2V_F32)
+    grad_h_init_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(
+        *sh, K, (const float *)dg, actions, (const float *)dact, (float *)grad_h);
+  else
+    grad_h_init_kernel<double><<<grid, 256, 0, as_stream(stream)>>>(
+        *sh, K, (const double *)dg, actions, (const double *)dact, (double *)grad_h);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_layer_backward(s2v_dtype dt, const s2v_shard *sh, int K, const void *theta4,
+                       const void *grad_h, const void *h_l, const void *m_l, void *dzsum,
+                       void *partial, int first, void *dm_out, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  if (dt == S2V_F32)
+    return layer_backward_t<float>(sh, K, theta4, grad_h, h_l, m_l, dzsum, partial, first,
+                                   dm_out, st);
+  return layer_backward_t<double>(sh, K, theta4, grad_h, h_l, m_l, dzsum, partial, first, dm_out,
+                                  st);
+}
+
+int s2v_gather(s2v_dtype dt, const s2v_shard *sh, int K, const void *src, void *out,
+               void *stream) {
+  int64_t rows = (int64_t)sh->batch * sh->num_rows;
+  if (rows == 0) return S2V_OK;
+  int grid = (int)std::min<int64_t>((rows * 32 + 255) / 256, kNumSMs * 16);
+  if (dt == S2V_F32)
+    gather_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(*sh, K, (const float *)src,
+                                                              (float *)out);
+  else
+    gather_kernel<double><<<grid, 256, 0, as_stream(stream)>>>(*sh, K, (const double *)src,
+                                                               (double *)out);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_param_grads(s2v_dtype dt, const s2v_shard *sh, int K, const void *theta2,
+                    const void *theta3, const void *dzsum, void *partials, void *stream) {
+  if (2 * K + K * K > 72 * kBwdThreads) return fail(S2V_EINVAL, "embed_dim %d too large", K);
+  size_t elem = dt == S2V_F32 ? 4 : 8;
+  size_t smem = elem * ((size_t)K * (K + 1) + 2 * kBwdTile * (size_t)K + 2 * kBwdTile);
+  cudaStream_t st = as_stream(stream);
+  if (dt == S2V_F32) {
+    auto kern = param_grads_kernel<float>;
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<bwd_blocks(*sh), kBwdThreads, smem, st>>>(*sh, K, (const float *)theta2,
+                                                     (const float *)theta3,
+                                                     (const float *)dzsum, (float *)partials);
+  } else {
+    auto kern = param_grads_kernel<double>;
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<bwd_blocks(*sh), kBwdThreads, smem, st>>>(*sh, K, (const double *)theta2,
+                                                     (const double *)theta3,
+                                                     (const double *)dzsum, (double *)partials);
+  }
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_reduce_partials(s2v_dtype dt, const void *partials, int nparts, int len, double *out,
+                        void *stream) {
+  int grid = (len + 255) / 256;
+  if (dt == S2V_F32)
+    reduce_partials_kernel<float><<<grid, 256, 0, as_stream(stream)>>>((const float *)partials,
+                                                                       nparts, len, out);
+  else
+    reduce_partials_kernel<double><<<grid, 256, 0, as_stream(stream)>>>(
+        (const double *)partials, nparts, len, out);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_head_backward(s2v_dtype dt, const s2v_shard *sh, int K, const void *h_L, const void *g,
+                      const int64_t *actions, const void *targets, const void *theta5,
+                      const void *theta6, const void *theta7, double *head_out, void *dg,
+                      void *dact, void *stream) {
+  size_t elem = dt == S2V_F32 ? 4 : 8;
+  size_t smem = elem * 6 * (size_t)K;
+  cudaStream_t st = as_stream(stream);
+  if (dt == S2V_F32)
+    head_backward_kernel<float><<<sh->batch, 128, smem, st>>>(
+        *sh, K, (const float *)h_L, (const float *)g, actions, (const float *)targets,
+        (const float *)theta5, (const float *)theta6, (const float *)theta7, head_out,
+        (float *)dg, (float *)dact);
+  else
+    head_backward_kernel<double><<<sh->batch, 128, smem, st>>>(
+        *sh, K, (const double *)h_L, (const double *)g, actions, (const double *)targets,
+        (const double *)theta5, (const double *)theta6, (const double *)theta7, head_out,
+        (double *)dg, (double *)dact);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_adam(s2v_dtype dt, void *params, const void *grads, void *m, void *v, int64_t n,
+             double beta1, double omb1, double beta2, double omb2, double eps, double lr,
+             double b1c, double b2c, void *stream) {
+  if (n == 0) return S2V_OK;
+  int grid = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 4);
+  if (dt == S2V_F32)
+    adam_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(
+        (float *)params, (const float *)grads, (float *)m, (float *)v, n, (float)beta1,
+        (float)omb1, (float)beta2, (float)omb2, (float)eps, (float)lr, (float)b1c, (float)b2c);
+  else
+    adam_kernel<double><<<grid, 256, 0, as_stream(stream)>>>(
+        (double *)params, (const double *)grads, (double *)m, (double *)v, n, beta1, omb1,
+        beta2, omb2, eps, lr, b1c, b2c);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+}  // extern "C"

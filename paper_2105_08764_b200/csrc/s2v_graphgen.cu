@@ -1,0 +1,136 @@
+// Native graph ingestion (host code): a Barabasi-Albert generator that
+// reproduces the reference's numpy draw sequence bit for bit.
+//
+// Replaces generate_ba (pkg/src/graphrl/graphs.py:125-157), which draws each
+// target with Generator.integers(len(repeated)) on a PCG64 stream.  numpy's
+// bounded draw for ranges < 2^32 is Lemire's method on the bit generator's
+// buffered 32-bit output (PCG64 next_uint32: low half of a 64-bit draw, high
+// half kept for the next call); that is reproduced here from the bit
+// generator state numpy's SeedSequence produced (passed in by the host).
+// Output: the E = C(d,2) + d(n-d) edges (u < v), lexicographically sorted,
+// exactly Graph(n, edges).edge_array of the reference.
+#include <stdint.h>
+
+#include <cstring>
+#include <vector>
+
+namespace {
+
+struct Pcg64 {
+  unsigned __int128 state, inc;
+  int has32;
+  uint32_t u32;
+  uint64_t next64() {
+    const unsigned __int128 mult =
+        ((unsigned __int128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+    state = state * mult + inc;
+    uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+    uint64_t x = hi ^ lo;
+    unsigned rot = (unsigned)(hi >> 58);
+    return (x >> rot) | (x << ((64 - rot) & 63));
+  }
+  uint32_t next32() {
+    if (has32) {
+      has32 = 0;
+      return u32;
+    }
+    uint64_t n = next64();
+    has32 = 1;
+    u32 = (uint32_t)(n >> 32);
+    return (uint32_t)n;
+  }
+  // Generator.integers(0, n) for 1 <= n <= 2^32 - 1 (numpy random_bounded_uint64_fill)
+  uint64_t bounded(uint64_t n) {
+    uint32_t rng = (uint32_t)(n - 1);
+    if (rng == 0) return 0;
+    uint32_t excl = rng + 1;
+    uint64_t m = (uint64_t)next32() * excl;
+    uint32_t left = (uint32_t)m;
+    if (left < excl) {
+      uint32_t th = (UINT32_MAX - rng) % excl;
+      while (left < th) {
+        m = (uint64_t)next32() * excl;
+        left = (uint32_t)m;
+      }
+    }
+    return m >> 32;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+// pcg: {state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger}.
+// edges_out: NULL to query the edge count, else [E][2] int64.  Returns E or -1.
+int64_t s2v_generate_ba(int64_t n, int64_t d, const void *pcg, void *edges_out) {
+  if (d < 1 || n <= d) return -1;
+  const int64_t E = d * (d - 1) / 2 + d * (n - d);
+  if (!edges_out) return E;
+  const uint64_t *p = (const uint64_t *)pcg;
+  Pcg64 g;
+  g.state = ((unsigned __int128)p[0] << 64) | p[1];
+  g.inc = ((unsigned __int128)p[2] << 64) | p[3];
+  g.has32 = (int)p[4];
+  g.u32 = (uint32_t)p[5];
+  if (2 * E >= (int64_t)UINT32_MAX) return -1;
+  std::vector<int32_t> eu, ev;
+  eu.reserve(E);
+  ev.reserve(E);
+  std::vector<int32_t> repeated;
+  repeated.reserve(2 * E);
+  for (int64_t i = 0; i < d; i++)
+    for (int64_t j = i + 1; j < d; j++) {
+      eu.push_back((int32_t)i);
+      ev.push_back((int32_t)j);
+      repeated.push_back((int32_t)i);
+      repeated.push_back((int32_t)j);
+    }
+  std::vector<int32_t> chosen(d);
+  for (int64_t node = d; node < n; node++) {
+    int64_t cnt = 0;
+    if (node == d) {
+      for (int64_t t = 0; t < d; t++) chosen[cnt++] = (int32_t)t;
+    } else {
+      while (cnt < d) {
+        int32_t t = repeated[g.bounded(repeated.size())];
+        bool dup = false;
+        for (int64_t q = 0; q < cnt; q++)
+          if (chosen[q] == t) {
+            dup = true;
+            break;
+          }
+        if (!dup) chosen[cnt++] = t;
+      }
+      // sorted(chosen): insertion sort (d is small)
+      for (int64_t a = 1; a < cnt; a++) {
+        int32_t x = chosen[a];
+        int64_t b = a - 1;
+        while (b >= 0 && chosen[b] > x) {
+          chosen[b + 1] = chosen[b];
+          b--;
+        }
+        chosen[b + 1] = x;
+      }
+    }
+    for (int64_t q = 0; q < cnt; q++) {
+      eu.push_back(chosen[q]);
+      ev.push_back((int32_t)node);
+      repeated.push_back(chosen[q]);
+      repeated.push_back((int32_t)node);
+    }
+  }
+  // stable counting sort by u: v's of a fixed u already appear ascending
+  std::vector<int64_t> start(n + 1, 0);
+  for (int64_t e = 0; e < E; e++) start[eu[e] + 1]++;
+  for (int64_t u = 0; u < n; u++) start[u + 1] += start[u];
+  int64_t *out = (int64_t *)edges_out;
+  for (int64_t e = 0; e < E; e++) {
+    int64_t pos = start[eu[e]]++;
+    out[2 * pos] = eu[e];
+    out[2 * pos + 1] = ev[e];
+  }
+  return E;
+}
+
+}  // extern "C"

@@ -1,0 +1,403 @@
+"""structure2vec-DQN policy: parameters, forward, exact gradients, Adam.
+
+API mirrors pkg/src/graphrl/policy.py.  Numerics run in libs2v (sm_100a):
+
+* embed_forward  -> s2v_e12_table + L x s2v_embed_round (+ halo all-gather of
+  the new rows over NCCL between rounds when P > 1);
+* q_forward      -> s2v_colsum (numpy pairwise order) + u1 = g @ theta5.T +
+  s2v_score;
+* loss_and_gradients / adam_step -> s2v_layer_backward, s2v_gather,
+  s2v_head_backward, s2v_param_grads, s2v_adam.
+
+Results are bit-identical to the reference's fp32 forward:
+embeddings, Q-values and selections match the CPU oracle exactly at any P.
+u1 = g @ theta5.T (B x K by K x K, 4K*B flops) is computed on the host with
+numpy, in the reference's own BLAS call, because OpenBLAS' small-matrix/gemv
+accumulation order for it is not a simple chain; it costs one
+256-byte round trip per evaluation.
+"""
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import ptr, stream_ptr
+from .errors import DataError
+from .state import PartitionedState
+
+PARAM_NAMES = ("theta1", "theta2", "theta3", "theta4", "theta5", "theta6", "theta7")
+
+_CKPT_MAGIC = b"GRLP"
+_CKPT_VERSION = 1
+_DTYPE_CODES = {np.dtype(np.float32): 0, np.dtype(np.float64): 1}
+_CODE_DTYPES = {v: k for k, v in _DTYPE_CODES.items()}
+
+
+def param_shapes(k: int) -> dict[str, tuple[int, int]]:
+    return {"theta1": (k, 1), "theta2": (k, 1), "theta3": (k, k), "theta4": (k, k),
+            "theta5": (k, k), "theta6": (k, k), "theta7": (2 * k, 1)}
+
+
+@dataclass
+class PolicyParams:
+    """The seven trainable matrices plus depth L (policy.py:43-113)."""
+    theta1: np.ndarray
+    theta2: np.ndarray
+    theta3: np.ndarray
+    theta4: np.ndarray
+    theta5: np.ndarray
+    theta6: np.ndarray
+    theta7: np.ndarray
+    num_layers: int
+
+    @property
+    def embed_dim(self) -> int:
+        return self.theta1.shape[0]
+
+    @property
+    def dtype(self) -> np.dtype:
+        return self.theta1.dtype
+
+    def __post_init__(self):
+        self.validate()
+
+    def validate(self) -> None:
+        expected = param_shapes(self.theta1.shape[0])
+        for name in PARAM_NAMES:
+            arr = getattr(self, name)
+            if arr.shape != expected[name]:
+                raise ValueError(f"{name} must have shape {expected[name]}, got {arr.shape}")
+            if not np.all(np.isfinite(arr)):
+                raise ValueError(f"{name} contains non-finite entries")
+        if self.num_layers < 1:
+            raise ValueError(f"num_layers must be >= 1, got {self.num_layers}")
+
+    @classmethod
+    def initialize(cls, embed_dim: int, num_layers: int, seed: int, scale: float = 0.05,
+                   dtype=np.float32, orientation: str = "positive") -> "PolicyParams":
+        """Seeded uniform init with the reference's draw order (policy.py:79-102)."""
+        if orientation not in ("positive", "symmetric"):
+            raise ValueError(f"unknown init orientation {orientation!r}")
+        rng = np.random.default_rng(seed)
+        shapes = param_shapes(embed_dim)
+        arrays = {name: rng.uniform(-scale, scale, shapes[name]).astype(dtype)
+                  for name in PARAM_NAMES}
+        if orientation == "positive":
+            arrays["theta6"] = np.abs(arrays["theta6"])
+            arrays["theta7"][embed_dim:] = np.abs(arrays["theta7"][embed_dim:])
+        return cls(num_layers=num_layers, **arrays)
+
+    def astype(self, dtype) -> "PolicyParams":
+        return PolicyParams(num_layers=self.num_layers,
+                            **{n: getattr(self, n).astype(dtype) for n in PARAM_NAMES})
+
+    def copy(self) -> "PolicyParams":
+        return self.astype(self.dtype)
+
+    def as_dict(self) -> dict[str, np.ndarray]:
+        return {name: getattr(self, name) for name in PARAM_NAMES}
+
+
+def zero_grads(params: PolicyParams) -> dict[str, np.ndarray]:
+    return {name: np.zeros_like(getattr(params, name)) for name in PARAM_NAMES}
+
+
+def flatten_arrays(arrays: dict[str, np.ndarray]) -> np.ndarray:
+    return np.concatenate([arrays[name].ravel() for name in PARAM_NAMES])
+
+
+def unflatten_arrays(vec: np.ndarray, k: int) -> dict[str, np.ndarray]:
+    out, off = {}, 0
+    for name, shp in param_shapes(k).items():
+        size = shp[0] * shp[1]
+        out[name] = vec[off:off + size].reshape(shp).copy()
+        off += size
+    return out
+
+
+def _dt_code(dtype) -> int:
+    dt = np.dtype(dtype)
+    if dt == np.float32:
+        return _lib.S2V_F32
+    if dt == np.float64:
+        return _lib.S2V_F64
+    raise ValueError(f"unsupported dtype {dt}")
+
+
+def _torch_dtype(dtype):
+    return torch.float32 if np.dtype(dtype) == np.float32 else torch.float64
+
+
+class _DeviceParams:
+    """The seven thetas packed in one device buffer (one H2D per call)."""
+
+    def __init__(self, params: PolicyParams, device):
+        flat = np.ascontiguousarray(flatten_arrays(params.as_dict()), dtype=params.dtype)
+        self.buf = torch.from_numpy(flat).to(device, non_blocking=False)
+        self.k = params.embed_dim
+        self.offsets = {}
+        off = 0
+        for name, shp in param_shapes(self.k).items():
+            self.offsets[name] = off
+            off += shp[0] * shp[1]
+        self.elem = flat.dtype.itemsize
+
+    def ptr(self, name: str) -> int:
+        return self.buf.data_ptr() + self.offsets[name] * self.elem
+
+
+def _check_dtype(state: PartitionedState, params: PolicyParams) -> None:
+    if np.dtype(params.dtype) not in _DTYPE_CODES:
+        raise ValueError(f"unsupported parameter dtype {params.dtype}")
+
+
+class DeviceEmbedding:
+    """Lazy (B, K, rows) view of embeddings resident in HBM.
+
+    Layout on device: node-major [B][P][rows_max][K]; materialised on the host
+    (numpy, reference layout) only when a caller reads it.
+    """
+
+    def __init__(self, state: PartitionedState, h: torch.Tensor, k: int, dtype,
+                 gathered: bool):
+        self.state = state
+        self.h = h
+        self.k = k
+        self.dtype = np.dtype(dtype)
+        self.gathered = gathered
+        self.shape = (state.batch, k, state.part.num_rows)
+        self.ndim = 3
+
+    def local_rows(self) -> torch.Tensor:
+        st = self.state
+        v = self.h.view(st.batch, st.world, st.rows_max, self.k)
+        return v[:, st.part.rank, :st.part.num_rows, :]
+
+    def __array__(self, dtype=None, copy=None):
+        arr = self.local_rows().to("cpu").numpy().transpose(0, 2, 1)
+        arr = np.ascontiguousarray(arr)
+        return arr.astype(dtype) if dtype is not None else arr
+
+    def __getitem__(self, idx):
+        return np.asarray(self)[idx]
+
+    def __len__(self):
+        return self.shape[0]
+
+
+def _buffers(state: PartitionedState, k: int, dtype, count: int):
+    n_el = state.batch * state.world * state.rows_max * k
+    tdt = _torch_dtype(dtype)
+
+    def make():
+        return [torch.zeros(n_el, dtype=tdt, device=state.device) for _ in range(count)]
+    return state.workspace(f"h{count}", (k, np.dtype(dtype).str, count), make)
+
+
+def _allgather_rows(state: PartitionedState, comm, h: torch.Tensor, k: int, tag: str):
+    """In-place halo all-gather of every slot's rank chunk (NCCL)."""
+    if state.world == 1:
+        return
+    dc = comm.device_comm()
+    chunk = state.rows_max * k * h.element_size()
+    dc.allgather_slots(h.data_ptr(), chunk, chunk * state.world, state.batch, stream_ptr())
+    comm.record(tag, state.rows_max * k * state.batch)
+
+
+def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers: int, comm,
+                    dtype, tape: bool):
+    """L embedding rounds.  Returns the list of h buffers (all of them when
+    tape, else the final one) and, when tape, the m buffers per round."""
+    k = dparams.k
+    dt = _dt_code(dtype)
+    st = stream_ptr()
+    max_deg = int(state.max_deg)
+    table = state.workspace("e12", (k, np.dtype(dtype).str, max_deg), lambda: torch.empty(
+        (max_deg + 2) * k, dtype=_torch_dtype(dtype), device=state.device))
+    _lib.call("s2v_e12_table", dt, dparams.ptr("theta1"), dparams.ptr("theta2"),
+              dparams.ptr("theta3"), k, max_deg, ptr(table), st)
+    if tape:
+        hs = _buffers(state, k, dtype, num_layers)
+        rows = state.batch * state.part.num_rows
+        ms = state.workspace("mtape", (k, np.dtype(dtype).str, num_layers), lambda: [
+            torch.empty(max(rows * k, 1), dtype=_torch_dtype(dtype), device=state.device)
+            for _ in range(num_layers)])
+    else:
+        hs = _buffers(state, k, dtype, 2)
+        ms = None
+    h_prev = None
+    out = []
+    for layer in range(num_layers):
+        h_out = hs[layer] if tape else hs[layer % 2]
+        m_out = ms[layer] if (tape and layer > 0) else None
+        _lib.call("s2v_embed_round", dt, state.shard_ref(), dparams.ptr("theta4"), ptr(table),
+                  k, max_deg, ptr(h_prev), ptr(h_out), ptr(m_out), st)
+        _allgather_rows(state, comm, h_out, k, "embed_fwd")
+        h_prev = h_out
+        out.append(h_out)
+    return out, ms, table
+
+
+def embed_forward(state: PartitionedState, params: PolicyParams, comm) -> DeviceEmbedding:
+    """(B, K, rows) embeddings of the locally owned nodes (policy.py:182-185)."""
+    _check_dtype(state, params)
+    dparams = _DeviceParams(params, state.device)
+    hs, _, _ = _forward_rounds(state, dparams, params.num_layers, comm, params.dtype, False)
+    return DeviceEmbedding(state, hs[-1], params.embed_dim, params.dtype, gathered=True)
+
+
+def _as_device_embedding(embed, state_hint, params: PolicyParams, comm) -> DeviceEmbedding:
+    if isinstance(embed, DeviceEmbedding):
+        return embed
+    raise TypeError("q_forward needs the DeviceEmbedding returned by embed_forward")
+
+
+def _global_sum(emb: DeviceEmbedding) -> np.ndarray:
+    """g = pairwise sum over all N nodes of every slot (policy.py:199-200)."""
+    st = emb.state
+    k = emb.k
+    wsb = _lib.load().s2v_colsum_workspace(st.shard_ref(), k, emb.dtype.itemsize)
+    ws = st.workspace("colsum", (k, emb.dtype.str), lambda: {
+        "ws": torch.empty(max(wsb // emb.dtype.itemsize, 1), dtype=_torch_dtype(emb.dtype),
+                          device=st.device),
+        "g": torch.empty(st.batch * k, dtype=_torch_dtype(emb.dtype), device=st.device)})
+    _lib.call("s2v_colsum", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h), ptr(ws["g"]),
+              ptr(ws["ws"]), wsb, stream_ptr())
+    return ws["g"].to("cpu").numpy().reshape(st.batch, k)
+
+
+def _score(emb: DeviceEmbedding, params: PolicyParams, dparams: _DeviceParams,
+           cand_override: np.ndarray | None, mode: int, d: int):
+    """Run the scorer; returns (scores device tensor, top keys (B,d,2) or None,
+    counts (B,))."""
+    st = emb.state
+    k = emb.k
+    g = _global_sum(emb)
+    # policy.py:201 -- the reference's own numpy product, on the host
+    u1 = np.ascontiguousarray(g @ params.theta5.T, dtype=params.dtype)
+    nblk = _lib.load().s2v_score_blocks(st.shard_ref())
+    rows = st.batch * st.part.num_rows
+    ws = st.workspace("score", (k, emb.dtype.str), lambda: {
+        "u1": torch.empty(st.batch * k, dtype=_torch_dtype(emb.dtype), device=st.device),
+        "scores": torch.empty(max(rows, 1), dtype=_torch_dtype(emb.dtype), device=st.device),
+        "bkeys": torch.empty(st.batch * nblk * 8 * 2, dtype=torch.int64, device=st.device),
+        "counts": torch.empty(st.batch, dtype=torch.int64, device=st.device),
+        "top": torch.empty(st.batch * 8 * 2, dtype=torch.int64, device=st.device),
+        "cand": torch.empty(max(rows, 1), dtype=torch.uint8, device=st.device)})
+    ws["u1"].copy_(torch.from_numpy(u1.reshape(-1)))
+    cand_ptr = None
+    if cand_override is not None:
+        ws["cand"][:rows].copy_(torch.from_numpy(
+            np.ascontiguousarray(cand_override, dtype=np.uint8).reshape(-1)))
+        cand_ptr = ptr(ws["cand"])
+    s = stream_ptr()
+    _lib.call("s2v_score", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h), ptr(ws["u1"]),
+              dparams.ptr("theta6"), dparams.ptr("theta7"), cand_ptr, mode,
+              ptr(ws["scores"]), ptr(ws["bkeys"]), ptr(ws["counts"]), s)
+    top = None
+    if d > 0:
+        _lib.call("s2v_topk_merge", st.shard_ref(), ptr(ws["bkeys"]), d, ptr(ws["top"]), s)
+        top = ws["top"][:st.batch * d * 2].to("cpu").numpy().view(np.uint64).reshape(
+            st.batch, d, 2)
+    counts = ws["counts"].to("cpu").numpy().copy()
+    return ws["scores"][:rows], top, counts
+
+
+def q_forward(embed, cand: np.ndarray, params: PolicyParams, comm) -> np.ndarray:
+    """(B, rows) scores for every locally owned node (policy.py:214-218).
+    `cand` is the sparse-diagonal extractor (non-candidates get a zeroed
+    own-embedding term); masking happens in masked_scores."""
+    emb = _as_device_embedding(embed, None, params, comm)
+    st = emb.state
+    dparams = _DeviceParams(params, st.device)
+    cand = np.asarray(cand)
+    override = None if cand is st.cand else cand
+    comm.record("q_fwd", st.batch * emb.k)
+    scores, _, _ = _score(emb, params, dparams, override, 0, 0)
+    return scores.to("cpu").numpy().reshape(st.batch, st.part.num_rows).astype(params.dtype)
+
+
+def masked_scores(scores: np.ndarray, cand: np.ndarray) -> np.ndarray:
+    """Scores with non-candidates pushed to -inf (policy.py:221-224)."""
+    neg = np.array(-np.inf, dtype=scores.dtype)
+    return np.where(cand.astype(bool), scores, neg)
+
+
+def decode_keys(top: np.ndarray):
+    """(..., 2) uint64 keys -> (node ids int64, scores float64, valid bool)."""
+    s = top[..., 0]
+    node = (~top[..., 1]).astype(np.int64)
+    valid = s != 0
+    sign = np.uint64(1) << np.uint64(63)
+    bits = np.where(s & sign, s & ~sign, ~s)
+    vals = bits.view(np.float64).copy()
+    vals[s == np.uint64(0xFFFFFFFFFFFFFFFF)] = np.nan
+    return node, vals, valid
+
+
+def evaluate(state: PartitionedState, params: PolicyParams, comm, d: int, mode: int = 0):
+    """Fused policy evaluation for the selection loops: embed + score + top-d
+    keys, nothing but keys and counts leave the device.  Returns
+    (nodes (B,d), scores (B,d), valid (B,d), counts (B,))."""
+    dparams = _DeviceParams(params, state.device)
+    hs, _, _ = _forward_rounds(state, dparams, params.num_layers, comm, params.dtype, False)
+    emb = DeviceEmbedding(state, hs[-1], params.embed_dim, params.dtype, gathered=True)
+    _, top, counts = _score(emb, params, dparams, None, mode, d)
+    if state.world > 1:
+        # merge per-rank top-d keys identically on every rank
+        keys = comm.all_gather(top.reshape(state.batch, -1), axis=-1, tag="select")
+        keys = keys.reshape(state.batch, -1, 2)
+        counts = comm.all_reduce_sum(counts, tag="select")
+        order = np.lexsort((keys[..., 1], keys[..., 0]), axis=-1)[:, ::-1][:, :d]
+        top = np.take_along_axis(keys, order[..., None], axis=1)
+    nodes, vals, valid = decode_keys(top)
+    return nodes, vals, valid, counts
+
+
+# ---------------------------------------------------------------------------
+# Checkpoints (policy.py:367-407): format unchanged
+# ---------------------------------------------------------------------------
+
+
+def save_checkpoint(params: PolicyParams, path) -> None:
+    path = Path(path)
+    code = _DTYPE_CODES.get(np.dtype(params.dtype))
+    if code is None:
+        raise ValueError(f"unsupported checkpoint dtype {params.dtype}")
+    with open(path, "wb") as fh:
+        fh.write(_CKPT_MAGIC)
+        fh.write(struct.pack("<III B", _CKPT_VERSION, params.embed_dim, params.num_layers, code))
+        for name in PARAM_NAMES:
+            fh.write(np.ascontiguousarray(getattr(params, name)).tobytes())
+
+
+def load_checkpoint(path) -> PolicyParams:
+    path = Path(path)
+    if not path.exists():
+        raise DataError(f"checkpoint not found: {path}")
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic != _CKPT_MAGIC:
+            raise DataError(f"{path}: not a policy checkpoint (magic {magic!r})")
+        version, k, layers, code = struct.unpack("<III B", fh.read(13))
+        if version != _CKPT_VERSION:
+            raise DataError(f"{path}: unsupported checkpoint version {version}")
+        if code not in _CODE_DTYPES:
+            raise DataError(f"{path}: unknown dtype code {code}")
+        dtype = _CODE_DTYPES[code]
+        arrays = {}
+        for name, shp in param_shapes(k).items():
+            nbytes = shp[0] * shp[1] * dtype.itemsize
+            buf = fh.read(nbytes)
+            if len(buf) != nbytes:
+                raise DataError(f"{path}: truncated checkpoint at {name}")
+            arrays[name] = np.frombuffer(buf, dtype=dtype).reshape(shp).copy()
+        if fh.read(1):
+            raise DataError(f"{path}: trailing bytes after parameters")
+    return PolicyParams(num_layers=layers, **arrays)

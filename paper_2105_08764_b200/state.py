@@ -1,0 +1,319 @@
+"""Device-resident residual graph state (one rank's row shard of B graphs).
+
+API mirrors pkg/src/graphrl/state.py (Partition, partition_rows,
+PartitionedState, apply_action, is_covered).  Where the reference keeps a
+scipy CSR whose removed entries are zeroed values, this keeps, in HBM:
+
+* row_ptr int64 [B*rows+1] and cols uint32 [nnz]: the local rows of every
+  slot, neighbour lists ascending, each entry holding the neighbour's physical
+  row in the embedding layout [B][P][rows_max] with bit 31 = removed;
+* the transpose lookup col_ptr/col_ent/col_row (state.py:115-122's
+  _col_order/_col_ptr) used to remove column v on every rank;
+* rdeg int32, sol/cand uint8, residual int64 [B].
+
+The structure of each graph is uploaded once per device and reused by every
+state built from it (tuples_to_graphs, batch_targets, env resets).  Host views
+(sol, cand, local_residual, local_degrees) are cached D2H mirrors, refreshed
+after every mutation.
+"""
+from __future__ import annotations
+
+import ctypes
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import current_device, ptr, stream_ptr, to_device
+from .errors import InvalidActionError
+from .graphs import Graph
+
+
+@dataclass(frozen=True)
+class Partition:
+    """The block of node rows owned by one rank (state.py:20-33)."""
+    rank: int
+    num_workers: int
+    row_start: int
+    row_stop: int
+
+    @property
+    def num_rows(self) -> int:
+        return self.row_stop - self.row_start
+
+    def owns(self, node: int) -> bool:
+        return self.row_start <= node < self.row_stop
+
+
+def partition_rows(n: int, p: int) -> list[Partition]:
+    """Balanced block partition of [0, n) over p ranks (state.py:36-53)."""
+    if p < 1:
+        raise ValueError(f"worker count must be >= 1, got {p}")
+    if p > n:
+        raise ValueError(f"more workers ({p}) than nodes ({n})")
+    base, extra = divmod(n, p)
+    parts, start = [], 0
+    for rank in range(p):
+        stop = start + base + (1 if rank < extra else 0)
+        parts.append(Partition(rank, p, start, stop))
+        start = stop
+    return parts
+
+
+def rows_max_of(n: int, p: int) -> int:
+    return -(-n // p)
+
+
+def phys_rows(n: int, p: int) -> np.ndarray:
+    """Physical row (slot 0) of every global node: r*rows_max + (u - start_r)."""
+    base, extra = divmod(n, p)
+    u = np.arange(n, dtype=np.int64)
+    big = extra * (base + 1)
+    r = np.where(u < big, u // (base + 1), extra + (u - big) // max(base, 1))
+    start = r * base + np.minimum(r, extra)
+    return r * rows_max_of(n, p) + (u - start)
+
+
+# -- per-(graph, device, partition) structure cache ---------------------------
+
+_STRUCT_CACHE: "weakref.WeakKeyDictionary[Graph, dict]" = weakref.WeakKeyDictionary()
+
+
+class _ShardStructure:
+    """One graph's local rows on one device: CSR + transpose lookup."""
+
+    def __init__(self, graph: Graph, part: Partition, device: torch.device):
+        n, p = graph.num_nodes, part.num_workers
+        row_ptr_g, cols_g = graph.csr_arrays()
+        lo, hi = int(row_ptr_g[part.row_start]), int(row_ptr_g[part.row_stop])
+        row_ptr = row_ptr_g[part.row_start:part.row_stop + 1] - lo
+        nbr = cols_g[lo:hi]
+        phys = phys_rows(n, p) if p > 1 else None
+        cols0 = (phys[nbr] if phys is not None else nbr).astype(np.int32)
+        rows = part.num_rows
+        local_row = np.repeat(np.arange(rows, dtype=np.int32), np.diff(row_ptr))
+        order = np.argsort(nbr, kind="stable")  # by column, rows ascending
+        col_ptr = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(np.bincount(nbr, minlength=n), out=col_ptr[1:])
+        self.nnz = hi - lo
+        self.rows = rows
+        self.max_deg = int(np.diff(row_ptr).max()) if rows else 0
+        self.row_ptr = to_device(row_ptr, device)
+        self.cols0 = to_device(cols0, device)
+        self.col_ptr = to_device(col_ptr, device)
+        self.col_ent = to_device(order.astype(np.int64), device)
+        self.col_row = to_device(local_row[order], device)
+
+
+def _structure(graph: Graph, part: Partition, device: torch.device) -> _ShardStructure:
+    per_graph = _STRUCT_CACHE.setdefault(graph, {})
+    key = (device.index, part.num_workers, part.rank)
+    st = per_graph.get(key)
+    if st is None:
+        st = _ShardStructure(graph, part, device)
+        per_graph[key] = st
+    return st
+
+
+class PartitionedState:
+    """One rank's slice of state for a batch of B graphs with equal N
+    (state.py:56-111), resident in HBM."""
+
+    def __init__(self, graphs: list[Graph], part: Partition,
+                 solutions: np.ndarray | None = None, dtype=np.float32,
+                 graph_ids: list[int] | None = None):
+        if not graphs:
+            raise ValueError("need at least one graph")
+        n = graphs[0].num_nodes
+        if any(g.num_nodes != n for g in graphs):
+            raise ValueError("all graphs in a batch must have the same node count")
+        batch = len(graphs)
+        self.part = part
+        self.num_nodes = n
+        self.batch = batch
+        self.graph_ids = list(graph_ids) if graph_ids is not None else list(range(batch))
+        self.dtype = np.dtype(dtype)
+        if solutions is None:
+            solutions = np.zeros((batch, n), dtype=np.uint8)
+        else:
+            solutions = np.asarray(solutions, dtype=np.uint8)
+            if solutions.shape != (batch, n):
+                raise ValueError(
+                    f"solutions must be (B, N) = ({batch}, {n}), got {solutions.shape}")
+        self.device = current_device()
+        dev = self.device
+        P = part.num_workers
+        self.world = P
+        self.rows_max = rows_max_of(n, P)
+        rows = part.num_rows
+        structs = [_structure(g, part, dev) for g in graphs]
+        self.max_deg = max(s.max_deg for s in structs)
+        ent_off = np.zeros(batch + 1, dtype=np.int64)
+        np.cumsum([s.nnz for s in structs], out=ent_off[1:])
+        self.nnz = int(ent_off[-1])
+        slot_stride = P * self.rows_max
+        # block-diagonal assembly over slots (device-to-device, structure cached)
+        rp = [s.row_ptr[:-1] + int(ent_off[b]) for b, s in enumerate(structs)]
+        rp.append(torch.tensor([self.nnz], dtype=torch.int64, device=dev))
+        self.row_ptr = torch.cat(rp)
+        self.cols = torch.cat([s.cols0 + int(b * slot_stride) if b else s.cols0.clone()
+                               for b, s in enumerate(structs)]) if self.nnz else \
+            torch.zeros(1, dtype=torch.int32, device=dev)
+        cp = [s.col_ptr[:-1] + int(ent_off[b]) for b, s in enumerate(structs)]
+        cp.append(torch.tensor([self.nnz], dtype=torch.int64, device=dev))
+        self.col_ptr = torch.cat(cp)
+        self.col_ent = torch.cat([s.col_ent + int(ent_off[b]) for b, s in enumerate(structs)]) \
+            if self.nnz else torch.zeros(1, dtype=torch.int64, device=dev)
+        self.col_row = torch.cat([s.col_row + int(b * rows) for b, s in enumerate(structs)]) \
+            if self.nnz else torch.zeros(1, dtype=torch.int32, device=dev)
+        nr = max(batch * rows, 1)
+        self.rdeg = torch.zeros(nr, dtype=torch.int32, device=dev)
+        self.sol_d = torch.zeros(nr, dtype=torch.uint8, device=dev)
+        self.cand_d = torch.zeros(nr, dtype=torch.uint8, device=dev)
+        self.residual_d = torch.zeros(batch, dtype=torch.int64, device=dev)
+        self._shard = _lib.s2v_shard(
+            num_nodes=n, batch=batch, world=P, rank=part.rank, _pad=0,
+            row_start=part.row_start, num_rows=rows, rows_max=self.rows_max, nnz=self.nnz,
+            row_ptr=ptr(self.row_ptr), cols=ptr(self.cols), col_ptr=ptr(self.col_ptr),
+            col_ent=ptr(self.col_ent), col_row=ptr(self.col_row), rdeg=ptr(self.rdeg),
+            sol=ptr(self.sol_d), cand=ptr(self.cand_d), residual=ptr(self.residual_d))
+        sol_phys = np.zeros((batch, P, self.rows_max), dtype=np.uint8)
+        if P == 1:
+            sol_phys[:, 0, :] = solutions
+        else:
+            for r, pr in enumerate(partition_rows(n, P)):
+                sol_phys[:, r, :pr.num_rows] = solutions[:, pr.row_start:pr.row_stop]
+        sol_phys_d = to_device(sol_phys.reshape(-1), dev)
+        _lib.call("s2v_shard_init", ctypes.byref(self._shard), ptr(sol_phys_d), stream_ptr())
+        self._host = {}
+        self._ws: dict = {}
+
+    # -- C view ------------------------------------------------------------
+
+    @property
+    def shard(self) -> ctypes.Structure:
+        return self._shard
+
+    def shard_ref(self):
+        return ctypes.byref(self._shard)
+
+    def workspace(self, name: str, key, make):
+        """Per-state cache of device scratch buffers (reused across steps)."""
+        entry = self._ws.get(name)
+        if entry is None or entry[0] != key:
+            entry = (key, make())
+            self._ws[name] = entry
+        return entry[1]
+
+    def invalidate(self) -> None:
+        self._host.clear()
+
+    def _mirror(self, name: str, tensor: torch.Tensor, shape) -> np.ndarray:
+        arr = self._host.get(name)
+        if arr is None:
+            arr = tensor.to("cpu").numpy()[:int(np.prod(shape))].reshape(shape)
+            self._host[name] = arr
+        return arr
+
+    # -- views (state.py:140-155) -------------------------------------------
+
+    @property
+    def sol(self) -> np.ndarray:
+        return self._mirror("sol", self.sol_d, (self.batch, self.part.num_rows))
+
+    @property
+    def cand(self) -> np.ndarray:
+        return self._mirror("cand", self.cand_d, (self.batch, self.part.num_rows))
+
+    @property
+    def local_residual(self) -> np.ndarray:
+        return self._mirror("residual", self.residual_d, (self.batch,))
+
+    def local_degrees(self) -> np.ndarray:
+        """(B, rows) residual degree of each locally owned node."""
+        deg = self._mirror("rdeg", self.rdeg, (self.batch, self.part.num_rows))
+        return deg.astype(self.dtype)
+
+    def local_residual_coo(self, slot: int) -> tuple[np.ndarray, np.ndarray]:
+        """Surviving (global row, col) entries of one graph's local slice."""
+        rows = self.part.num_rows
+        rp = self.row_ptr.to("cpu").numpy()
+        lo, hi = int(rp[slot * rows]), int(rp[(slot + 1) * rows])
+        cols = (self.cols[lo:hi].to("cpu").numpy().view(np.uint32) if hi > lo
+                else np.zeros(0, np.uint32))
+        alive = (cols & np.uint32(0x80000000)) == 0
+        phys = (cols & np.uint32(0x7FFFFFFF)).astype(np.int64)
+        local_rows = np.repeat(np.arange(rows), np.diff(rp[slot * rows:(slot + 1) * rows + 1]))
+        inv = np.empty(self.world * self.rows_max, dtype=np.int64)
+        inv.fill(-1)
+        inv[phys_rows(self.num_nodes, self.world)] = np.arange(self.num_nodes)
+        slot_phys = phys - slot * self.world * self.rows_max
+        return (local_rows[alive] + self.part.row_start, inv[slot_phys[alive]])
+
+    # -- mutation (state.py:173-208) -------------------------------------------
+
+    def apply_action(self, v: int, slot: int = 0) -> None:
+        """Move node v into the partial solution of one batched graph.
+        Validation is owner-side, with the reference's messages."""
+        if not 0 <= v < self.num_nodes:
+            raise InvalidActionError(f"node {v} out of range [0, {self.num_nodes})")
+        if not 0 <= slot < self.batch:
+            raise InvalidActionError(f"batch slot {slot} out of range")
+        if self.part.owns(v):
+            i = v - self.part.row_start
+            if self.sol[slot, i]:
+                raise InvalidActionError(f"node {v} is already in the solution")
+            if not self.cand[slot, i]:
+                raise InvalidActionError(f"node {v} is not a candidate")
+        picks = np.full((self.batch, 1), -1, dtype=np.int64)
+        picks[slot, 0] = v
+        self.apply_groups(picks, comm=None)
+
+    def apply_groups(self, picks: np.ndarray, comm=None):
+        """Apply a group of picks per slot with the mid-group skip rule
+        (inference.py:125-146).  picks: (B, d) int64, -1 padded.  Returns
+        (applied (B, d) bool, removed (B,) global entries removed)."""
+        picks = np.ascontiguousarray(picks, dtype=np.int64)
+        B, d = picks.shape
+        ws = self.workspace("apply", d, lambda: {
+            "picks": torch.empty(B * d, dtype=torch.int64, device=self.device),
+            "info": torch.empty(2 * B * d, dtype=torch.int64, device=self.device),
+            "applied": torch.empty(B * d, dtype=torch.uint8, device=self.device),
+            "removed": torch.empty(B, dtype=torch.int64, device=self.device)})
+        ws["picks"].copy_(torch.from_numpy(picks.reshape(-1)), non_blocking=False)
+        st = stream_ptr()
+        _lib.call("s2v_apply_phase1", self.shard_ref(), ptr(ws["picks"]), d, ptr(ws["info"]), 0,
+                  None, st)
+        if self.world > 1 and d > 1:
+            dc = comm.device_comm() if comm is not None else None
+            if dc is None:
+                raise InvalidActionError("a sharded state needs its comm to apply picks")
+            dc.allreduce(ptr(ws["info"]), ws["info"].numel(), 0, st)
+        _lib.call("s2v_apply_phase2", self.shard_ref(), ptr(ws["picks"]), d, ptr(ws["info"]),
+                  ptr(ws["applied"]), ptr(ws["removed"]), st)
+        self.invalidate()
+        applied = ws["applied"].to("cpu").numpy().reshape(B, d).astype(bool)
+        removed = ws["removed"].to("cpu").numpy().copy()
+        return applied, removed
+
+    # -- termination (state.py:212-220) ------------------------------------------
+
+    def residual_counts(self, comm) -> np.ndarray:
+        """(B,) global residual adjacency entry counts (sum-all-reduce)."""
+        return comm.all_reduce_sum(self.local_residual, tag="env")
+
+    def is_covered(self, slot: int, comm) -> bool:
+        if not 0 <= slot < self.batch:
+            raise InvalidActionError(f"batch slot {slot} out of range")
+        return int(self.residual_counts(comm)[slot]) == 0
+
+
+def apply_action(state: PartitionedState, v: int, slot: int = 0) -> PartitionedState:
+    state.apply_action(v, slot)
+    return state
+
+
+def is_covered(state: PartitionedState, slot: int, comm) -> bool:
+    return state.is_covered(slot, comm)

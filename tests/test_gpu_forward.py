@@ -1,0 +1,41 @@
+"""GPU parity of the forward path against the C++ op-order oracle (bitwise)."""
+import numpy as np
+import pytest
+
+import paper_2105_08764_b200 as P
+from oracle import cref
+
+pytestmark = pytest.mark.gpu
+
+
+def _forward_gpu(g, params, sol=None):
+    def worker(comm):
+        part = P.partition_rows(g.num_nodes, comm.size)[comm.rank]
+        st = P.PartitionedState([g], part, solutions=None if sol is None else sol[None],
+                                dtype=params.dtype)
+        emb = P.embed_forward(st, params, comm)
+        h = np.asarray(emb)[0].T.copy()
+        sc = P.q_forward(emb, st.cand, params, comm)[0]
+        return h, sc, st.cand[0].copy()
+    return P.run_workers(1, worker)[0]
+
+
+@pytest.mark.parametrize("n,m,K,L,seed,solfrac,dtype", [
+    (1000, 4, 64, 5, 0, 0.0, np.float32),
+    (1000, 4, 64, 5, 0, 0.1, np.float32),
+    (800, 4, 32, 2, 1, 0.05, np.float32),
+    (300, 3, 8, 3, 2, 0.1, np.float32),
+    (500, 5, 16, 4, 3, 0.1, np.float64),
+    (3000, 8, 64, 5, 4, 0.2, np.float32),
+])
+def test_forward_bitwise_vs_oracle(n, m, K, L, seed, solfrac, dtype):
+    g = P.generate_ba(n, m, seed)
+    params = P.PolicyParams.initialize(K, L, seed=seed, dtype=dtype)
+    rng = np.random.default_rng(seed)
+    sol = (rng.random(n) < solfrac).astype(np.uint8)
+    h_gpu, s_gpu, cand_gpu = _forward_gpu(g, params, sol)
+    rp, cols = g.csr_arrays()
+    h, gsum, u1, cand, sc = cref.forward(rp, cols, sol, params.as_dict(), L, dtype=dtype)
+    assert np.array_equal(cand_gpu, cand)
+    assert np.array_equal(h_gpu, h), np.abs(h_gpu - h).max()
+    assert np.array_equal(s_gpu, sc), np.abs(s_gpu - sc).max()
