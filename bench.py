@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""Benchmark: one MVC structure2vec-DQN inference step on the >30M-edge
+Barabasi-Albert graph (BASELINE.json configs[2]: BA(2M, 16), K=64, T=5),
+node-sharded over N GPUs (one process per GPU under torchrun).
+
+A step = one policy evaluation (5 embedding rounds, pairwise global sum, Q
+scores, adaptive top-d keys) + selection + group apply -- one iteration of
+the reference's _solve_batch loop (pkg/src/graphrl/inference.py:107-147).
+Consecutive steps walk the episode from S = {} (the state evolves as in a
+real solve).  `value` is device time per step with the graph resident in HBM;
+`e2e` rebuilds the state from a host solution vector each step (H2D inside
+the timed region) through the public PartitionedState + solve_step API.
+
+--impl reference times the reference algorithm's CPU implementation
+(oracle/port.py: the reference's numpy/scipy calls, restated) on the host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "RL inference step time on 30M-edge BA graph (s)"
+MEASURED = ROOT / "MEASURED_PEAKS.json"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nodes", type=int, default=2_000_000)
+    ap.add_argument("--m", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    return {"workload": f"MVC inference step, BA({args.nodes},{args.m},seed=0), K=64, T=5, "
+                        f"adaptive 8/4/2/1, node-sharded",
+            "graph": f"generate_ba({args.nodes}, {args.m}, 0)", "embed_dim": 64, "rounds": 5,
+            "l2": "inputs larger than L2 (512 MB embedding buffers, 256 MB CSR)",
+            "parallelism": f"node-rows x{args.gpus}"}
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" +
+                                      self.FIELDS, "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        d = json.loads(MEASURED.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm / cpu_baseline
+# ---------------------------------------------------------------------------
+
+
+def cpu_state(graph):
+    from oracle import port
+    t0 = time.perf_counter()
+    st = port.ResidualState([graph.edge_array], graph.num_nodes, dtype=np.float32)
+    return st, time.perf_counter() - t0
+
+
+def cpu_sample(st, theta, layers=5):
+    """One bounded sample of the reference algorithm's inference step on the
+    same graph: one full embedding round (spmm + theta4 + relu) timed, times
+    the 5 rounds of a step, plus q_forward + masked select + group apply.
+    Returns (estimated step seconds, detail)."""
+    from oracle import port
+    t0 = time.perf_counter()
+    h1 = port.embed(st, theta, 1)
+    t_round = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    s = port.scores(h1, st.cand, theta)
+    gl = port.masked(s, st.cand)
+    cm = np.isfinite(gl[0])
+    picks = port.select_top_d(gl[0], cm, port.d_for(int(cm.sum()), st.n))
+    for j, v in enumerate(picks):
+        if j > 0 and not st.cand[0, v]:
+            continue
+        st.apply(v, 0)
+    t_rest = time.perf_counter() - t0
+    est = layers * t_round + t_rest
+    return est, {"round_s": round(t_round, 3), "q_select_apply_s": round(t_rest, 3)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2105_08764_b200.graphs as G
+    from paper_2105_08764_b200.policy import PolicyParams
+    graph = G.generate_ba(args.nodes, args.m, 0)
+    theta = PolicyParams.initialize(64, 5, seed=0).as_dict()
+    cores = os.cpu_count()
+    st, build = cpu_state(graph)
+    for _ in range(args.warmup):
+        cpu_sample(st, theta)
+    vals, detail = [], None
+    for _ in range(args.steps):
+        v, detail = cpu_sample(st, theta)
+        vals.append(v)
+    value = float(np.mean(vals))
+    sample = ("reference algorithm (oracle/port.py, numpy/scipy restatement of graphrl) "
+              "on the same graph: per step, 1 timed embedding round x 5 + q_forward + "
+              f"select + apply; {detail}; state build {build:.1f}s excluded")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload(args),
+            "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import paper_2105_08764_b200 as P
+    from paper_2105_08764_b200 import _lib, policy
+    from paper_2105_08764_b200.device import bind_device
+    from paper_2105_08764_b200.inference import solve_step
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    bind_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = P.DistComm()
+    else:
+        comm = P.WorkerGroup(1).comm(0)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    t0 = time.time()
+    graph = P.generate_ba(args.nodes, args.m, 0)
+    graph.csr_arrays()
+    t_gen = time.time() - t0
+    params = P.PolicyParams.initialize(64, 5, seed=0)
+    part = P.partition_rows(graph.num_nodes, world)[rank]
+    sched = P.SelectionSchedule.adaptive()
+    active = np.array([True])
+    t0 = time.time()
+    state = P.PartitionedState([graph], part)
+    torch.cuda.synchronize()
+    t_state = time.time() - t0
+
+    for _ in range(args.warmup):
+        solve_step(state, params, comm, sched, active)
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = _lib.launch_count
+    alive_entries = int(state.local_residual.sum())
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            solve_step(state, params, comm, sched, active)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+    step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    launches = _lib.launch_count - launches0
+
+    # roofline of the dominant kernel (the fused embedding round): per-launch
+    # CUDA events on the launching stream over one more step
+    policy.ROUND_TIMER = []
+    alive_now = int(state.local_residual.sum())
+    solve_step(state, params, comm, sched, active)
+    torch.cuda.synchronize()
+    rounds = policy.ROUND_TIMER
+    policy.ROUND_TIMER = None
+    round_ms = float(np.mean([a.elapsed_time(b) for a, b in rounds]))
+    rows = part.num_rows
+    nnz_loc = state.nnz
+    algo_bytes = 8 * (rows + 1) + 4 * nnz_loc + 256 * alive_now + 256 * rows + 4 * rows + rows
+    peak, peak_src = peaks()
+    achieved = algo_bytes / (round_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "kernel": "round64_kernel (fused gather-SpMM + theta4 FMA chain + e12 + relu)",
+                "round_ms": round(round_ms, 4), "algorithmic_bytes_per_launch": algo_bytes,
+                "peak_source": peak_src,
+                "bytes_model": "8(rows+1) row_ptr + 4 nnz cols + 256 alive gathers + 256 rows h_out"
+                               " + 4 rows rdeg + rows sol"}
+
+    # end to end through the public API: host solution vector -> state -> step
+    e2e = None
+    if not args.no_e2e:
+        sol_host = np.zeros((1, graph.num_nodes), dtype=np.uint8)
+        sol_host[0, part.row_start:part.row_stop] = state.sol[0]
+        if world > 1:
+            sol_host[0] = comm.all_reduce_sum(sol_host[0], tag="bench")
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            st2 = P.PartitionedState([graph], part, solutions=sol_host)
+            picks, applied = solve_step(st2, params, comm, sched, active)
+            for v, a in zip(picks[0], applied[0]):
+                if v >= 0 and a:
+                    sol_host[0, v] = 1
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_s = max_over_ranks(e0.elapsed_time(e1) / args.steps) / 1e3
+        params_bytes = sum(a.nbytes for a in params.as_dict().values())
+        e2e = {"value": e2e_s, "unit": "s",
+               "h2d_bytes_per_step": int(graph.num_nodes + params_bytes + 64 * 4 + 8 * 8),
+               "d2h_bytes_per_step": int(64 * 4 + 8 * 16 + 8 + 8 + 8),
+               "path": "PartitionedState(graphs, part, solutions=host S) + solve_step"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cst, build = cpu_state(graph)
+        est, detail = cpu_sample(cst, params.as_dict())
+        detail["state_build_s"] = round(build, 2)
+        cpu = {"value": est, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+               "sample": "oracle/port.py (reference numpy/scipy algorithm) on the same graph: "
+                         f"1 timed embedding round x 5 + q + select + apply; {detail}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": step_ms / 1e3, "unit": "s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic", "config": workload(args),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clocks.summary(),
+                "setup": {"graph_gen_s": round(t_gen, 2), "state_build_s": round(t_state, 3),
+                          "alive_entries_at_start": alive_entries}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

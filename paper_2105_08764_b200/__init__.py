@@ -5,13 +5,18 @@ step: the same public names and signatures, with the numerics in libs2v.so
 (hand-written CUDA for sm_100a behind a C ABI, include/s2v.h) and the node
 shards resident in HBM.  There is no CPU compute path.
 """
+from .agent import (ExperienceTuple, MetricsRow, ReplayBuffer, TrainConfig, act, batch_targets,
+                    compute_target, evaluate_ratio, pack_solution, train, train_step,
+                    tuples_to_graphs, unpack_solution)
 from .collective import Comm, CollectiveStats, DistComm, WorkerGroup, run_workers
+from .env import MVC, PROBLEMS, MvcEnv, ProblemSpec, reset
 from .errors import (CollectiveAborted, CollectiveError, ConfigError, DataError, GraphRLError,
                      InvalidActionError)
 from .graphs import Graph, generate_ba, generate_er, generate_rmat, load_edge_list, write_edge_list
 from .inference import SelectionSchedule, SolveResult, select_top_d, solve
-from .policy import (PolicyParams, embed_forward, load_checkpoint, masked_scores, q_forward,
-                     save_checkpoint)
+from .policy import (PARAM_NAMES, AdamState, PolicyParams, adam_step, embed_forward,
+                     load_checkpoint, loss_and_gradients, masked_scores, param_shapes, q_forward,
+                     save_checkpoint, zero_grads)
 from .state import Partition, PartitionedState, apply_action, is_covered, partition_rows
 
 __version__ = "0.1.0"

@@ -125,5 +125,17 @@ def check(rc: int, what: str = "") -> None:
     raise RuntimeError(f"libs2v CUDA failure: {text}")
 
 
+# kernels each entry point launches (for the bench's gpu_launches claim)
+KERNELS_PER_CALL = {
+    "s2v_shard_init": 1, "s2v_apply_phase1": 1, "s2v_apply_phase2": 1, "s2v_e12_table": 1,
+    "s2v_embed_round": 1, "s2v_colsum": 2, "s2v_score": 1, "s2v_topk_merge": 1,
+    "s2v_grad_h_init": 1, "s2v_layer_backward": 1, "s2v_gather": 1, "s2v_param_grads": 1,
+    "s2v_reduce_partials": 1, "s2v_head_backward": 1, "s2v_adam": 1,
+}
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
     check(getattr(load(), name)(*args), name)
+    launch_count += KERNELS_PER_CALL.get(name, 0)

@@ -210,6 +210,11 @@ def _allgather_rows(state: PartitionedState, comm, h: torch.Tensor, k: int, tag:
     comm.record(tag, state.rows_max * k * state.batch)
 
 
+# bench hook: when a list, every non-trivial round appends (start, end) CUDA
+# events recorded on the launching stream around its kernel
+ROUND_TIMER = None
+
+
 def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers: int, comm,
                     dtype, tape: bool):
     """L embedding rounds.  Returns the list of h buffers (all of them when
@@ -236,8 +241,16 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
     for layer in range(num_layers):
         h_out = hs[layer] if tape else hs[layer % 2]
         m_out = ms[layer] if (tape and layer > 0) else None
+        timer = ROUND_TIMER if (ROUND_TIMER is not None and h_prev is not None) else None
+        if timer is not None:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
         _lib.call("s2v_embed_round", dt, state.shard_ref(), dparams.ptr("theta4"), ptr(table),
                   k, max_deg, ptr(h_prev), ptr(h_out), ptr(m_out), st)
+        if timer is not None:
+            ev1.record()
+            timer.append((ev0, ev1))
         _allgather_rows(state, comm, h_out, k, "embed_fwd")
         h_prev = h_out
         out.append(h_out)
@@ -249,7 +262,9 @@ def embed_forward(state: PartitionedState, params: PolicyParams, comm) -> Device
     _check_dtype(state, params)
     dparams = _DeviceParams(params, state.device)
     hs, _, _ = _forward_rounds(state, dparams, params.num_layers, comm, params.dtype, False)
-    return DeviceEmbedding(state, hs[-1], params.embed_dim, params.dtype, gathered=True)
+    # a fresh buffer, like the reference's freshly allocated result (the
+    # workspace is reused by the next forward on this state)
+    return DeviceEmbedding(state, hs[-1].clone(), params.embed_dim, params.dtype, gathered=True)
 
 
 def _as_device_embedding(embed, state_hint, params: PolicyParams, comm) -> DeviceEmbedding:
@@ -358,6 +373,155 @@ def evaluate(state: PartitionedState, params: PolicyParams, comm, d: int, mode: 
         top = np.take_along_axis(keys, order[..., None], axis=1)
     nodes, vals, valid = decode_keys(top)
     return nodes, vals, valid, counts
+
+
+# ---------------------------------------------------------------------------
+# Loss and exact gradients (policy.py:232-315)
+# ---------------------------------------------------------------------------
+
+
+def loss_and_gradients(state: PartitionedState, actions, targets, params: PolicyParams, comm):
+    """MSE of Q(s_t, a_t) against targets with exact gradients.
+
+    Forward with tape (all h_l, m_l resident in HBM), Q head at the action
+    nodes on their owner rank, dg exchange, L-1 backward rounds (dm halo
+    exchange + alive-neighbour gather), theta1..theta4 reductions, one fp64
+    gradient pack (identical on every rank).  Returns (loss, grads)."""
+    b, n = state.batch, state.num_nodes
+    k = params.embed_dim
+    dtype = np.dtype(params.dtype)
+    actions = np.asarray(actions, dtype=np.int64)
+    targets = np.asarray(targets, dtype=dtype)
+    if actions.shape != (b,) or targets.shape != (b,):
+        raise ValueError(f"need {b} actions and targets, got {actions.shape} and {targets.shape}")
+    if not np.all(np.isfinite(targets)):
+        raise ValueError("targets must be finite")
+    if np.any(actions < 0) or np.any(actions >= n):
+        raise ValueError("action node index out of range")
+    _check_dtype(state, params)
+    dt = _dt_code(dtype)
+    tdt = _torch_dtype(dtype)
+    dev = state.device
+    s = stream_ptr()
+    L = params.num_layers
+    lib = _lib.load()
+    dparams = _DeviceParams(params, dev)
+    hs, ms, _ = _forward_rounds(state, dparams, L, comm, dtype, tape=True)
+    comm.record("q_fwd", b * k)
+    rows = state.batch * state.part.num_rows
+    nblk = lib.s2v_backward_blocks(state.shard_ref())
+    full = state.batch * state.world * state.rows_max * k
+    head_len = 2 * k * k + 2 * k + 1
+    plen = 2 * k + k * k
+    ws = state.workspace("bwd", (k, dtype.str, L), lambda: {
+        "actions": torch.empty(b, dtype=torch.int64, device=dev),
+        "targets": torch.empty(b, dtype=tdt, device=dev),
+        "head": torch.empty(b * head_len, dtype=torch.float64, device=dev),
+        "dg": torch.empty(b * k, dtype=tdt, device=dev),
+        "dact": torch.empty(b * k, dtype=tdt, device=dev),
+        "grad_h": torch.empty(max(rows * k, 1), dtype=tdt, device=dev),
+        "dzsum": torch.empty(max(rows * k, 1), dtype=tdt, device=dev),
+        "dm": torch.zeros(full, dtype=tdt, device=dev),
+        "p4": torch.empty(nblk * k * k, dtype=tdt, device=dev),
+        "pp": torch.empty(nblk * plen, dtype=tdt, device=dev),
+        "pack": torch.empty(4 * k * k + 4 * k + 1, dtype=torch.float64, device=dev)})
+    ws["actions"].copy_(torch.from_numpy(actions))
+    ws["targets"].copy_(torch.from_numpy(np.ascontiguousarray(targets)))
+    # g = pairwise sum of h_L (policy.py:199-200), kept on device
+    emb = DeviceEmbedding(state, hs[-1], k, dtype, gathered=True)
+    wsb = lib.s2v_colsum_workspace(state.shard_ref(), k, dtype.itemsize)
+    cs = state.workspace("colsum", (k, dtype.str), lambda: {
+        "ws": torch.empty(max(wsb // dtype.itemsize, 1), dtype=tdt, device=dev),
+        "g": torch.empty(b * k, dtype=tdt, device=dev)})
+    _lib.call("s2v_colsum", dt, state.shard_ref(), k, ptr(emb.h), ptr(cs["g"]), ptr(cs["ws"]),
+              wsb, s)
+    _lib.call("s2v_head_backward", dt, state.shard_ref(), k, ptr(hs[-1]), ptr(cs["g"]),
+              ptr(ws["actions"]), ptr(ws["targets"]), dparams.ptr("theta5"),
+              dparams.ptr("theta6"), dparams.ptr("theta7"), ptr(ws["head"]), ptr(ws["dg"]),
+              ptr(ws["dact"]), s)
+    dc = comm.device_comm() if state.world > 1 else None
+    if dc is not None:  # q_bwd: the adjoint of g reaches every rank's rows
+        dc.allreduce(ptr(ws["dg"]), b * k, 2 if dtype == np.float32 else 1, s)
+    comm.record("q_bwd", b * k)
+    _lib.call("s2v_grad_h_init", dt, state.shard_ref(), k, ptr(ws["dg"]), ptr(ws["actions"]),
+              ptr(ws["dact"]), ptr(ws["grad_h"]), s)
+    for layer in range(L - 1, -1, -1):
+        last = layer == 0
+        _lib.call("s2v_layer_backward", dt, state.shard_ref(), k, dparams.ptr("theta4"),
+                  ptr(ws["grad_h"]), ptr(hs[layer]), ptr(ms[layer]) if layer > 0 else None,
+                  ptr(ws["dzsum"]), ptr(ws["p4"]), 1 if layer == L - 1 else 0,
+                  None if last else ptr(ws["dm"]), s)
+        if last:
+            break
+        _allgather_rows(state, comm, ws["dm"], k, "embed_bwd")
+        _lib.call("s2v_gather", dt, state.shard_ref(), k, ptr(ws["dm"]), ptr(ws["grad_h"]), s)
+    _lib.call("s2v_param_grads", dt, state.shard_ref(), k, dparams.ptr("theta2"),
+              dparams.ptr("theta3"), ptr(ws["dzsum"]), ptr(ws["pp"]), s)
+    pack = ws["pack"]
+    base = pack.data_ptr()
+    _lib.call("s2v_reduce_partials", dt, ptr(ws["pp"]), nblk, plen, base, s)  # t1, t2, t3
+    _lib.call("s2v_reduce_partials", dt, ptr(ws["p4"]), nblk, k * k, base + 8 * plen, s)
+    _lib.call("s2v_reduce_partials", _lib.S2V_F64, ptr(ws["head"]), b, head_len,
+              base + 8 * (plen + k * k), s)  # t5, t6, t7, sq_err
+    if dc is not None:
+        dc.allreduce(base, pack.numel(), 1, s)
+    comm.record("grad", pack.numel())
+    reduced = pack.to("cpu").numpy()
+    grads = unflatten_arrays(reduced[:-1].astype(dtype), k)
+    return float(reduced[-1]) / b, grads
+
+
+# ---------------------------------------------------------------------------
+# Adam (policy.py:323-359)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class AdamState:
+    """First/second moments and step counter (policy.py:323-336)."""
+    m: dict
+    v: dict
+    step: int = 0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    lr: float = 1e-5
+
+    @classmethod
+    def create(cls, params: PolicyParams, lr: float = 1e-5) -> "AdamState":
+        return cls(m=zero_grads(params), v=zero_grads(params), lr=lr)
+
+
+def adam_step(params: PolicyParams, grads: dict, state: AdamState) -> None:
+    """One bias-corrected Adam update in place, on the device (s2v_adam);
+    non-finite gradients are rejected before any state changes."""
+    for name in PARAM_NAMES:
+        if not np.all(np.isfinite(grads[name])):
+            raise ValueError(f"non-finite gradient for {name}; step rejected")
+    dtype = np.dtype(params.dtype)
+    from .device import current_device
+    dev = current_device()
+    state.step += 1
+    b1c = 1.0 - state.beta1 ** state.step
+    b2c = 1.0 - state.beta2 ** state.step
+    k = params.embed_dim
+    packs = [np.ascontiguousarray(flatten_arrays(d), dtype=dtype)
+             for d in (params.as_dict(), grads, state.m, state.v)]
+    buf = torch.from_numpy(np.concatenate(packs)).to(dev)
+    n = packs[0].size
+    e = dtype.itemsize
+    p0 = buf.data_ptr()
+    _lib.call("s2v_adam", _dt_code(dtype), p0, p0 + n * e, p0 + 2 * n * e, p0 + 3 * n * e, n,
+              state.beta1, 1 - state.beta1, state.beta2, 1 - state.beta2, state.eps, state.lr,
+              b1c, b2c, stream_ptr())
+    out = buf.to("cpu").numpy()
+    new_p = unflatten_arrays(out[:n], k)
+    new_m = unflatten_arrays(out[2 * n:3 * n], k)
+    new_v = unflatten_arrays(out[3 * n:4 * n], k)
+    for name in PARAM_NAMES:
+        getattr(params, name)[...] = new_p[name]
+        state.m[name] = new_m[name]
+        state.v[name] = new_v[name]
 
 
 # ---------------------------------------------------------------------------

@@ -19,7 +19,6 @@ after every mutation.
 from __future__ import annotations
 
 import ctypes
-import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -78,9 +77,6 @@ def phys_rows(n: int, p: int) -> np.ndarray:
 
 # -- per-(graph, device, partition) structure cache ---------------------------
 
-_STRUCT_CACHE: "weakref.WeakKeyDictionary[Graph, dict]" = weakref.WeakKeyDictionary()
-
-
 class _ShardStructure:
     """One graph's local rows on one device: CSR + transpose lookup."""
 
@@ -108,7 +104,7 @@ class _ShardStructure:
 
 
 def _structure(graph: Graph, part: Partition, device: torch.device) -> _ShardStructure:
-    per_graph = _STRUCT_CACHE.setdefault(graph, {})
+    per_graph = graph._device_cache
     key = (device.index, part.num_workers, part.rank)
     st = per_graph.get(key)
     if st is None:

@@ -1,0 +1,94 @@
+"""Training path on the GPU vs the reference: golden losses/grads/params of a
+reference training step (tests/golden/train_*.npz) and the numpy port
+(oracle/port.py) on random cases; tolerance 1e-4 relative,
+Adam bitwise."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2105_08764_b200 as P
+from oracle import port
+from reference_math import scale_error
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.mark.parametrize("name,tol", [("train_ba1000_b4_k64_l5", 1e-4),
+                                      ("train_ba600_b3_k16_l3_f64", 1e-9)])
+def test_training_step_matches_reference(name, tol):
+    path = GOLD / f"{name}.npz"
+    if not path.exists():
+        pytest.skip("golden fixture not generated")
+    z = np.load(path)
+    n, m, B, K, L, tau = (int(z[k]) for k in ("n", "m", "B", "K", "L", "tau"))
+    dtype = z["p0_theta1"].dtype
+    dataset = [P.generate_ba(n, m, 100 + i) for i in range(B)]
+    params = P.PolicyParams(num_layers=L, **{k: z[f"p0_{k}"].copy() for k in P.PARAM_NAMES})
+    batch = [P.ExperienceTuple(i, P.pack_solution(z["snaps"][i]), int(z["actions"][i]), 0.0)
+             for i in range(B)]
+
+    def worker(comm):
+        part = P.partition_rows(n, 1)[0]
+        adam = P.AdamState.create(params, lr=1e-5)
+        state = P.tuples_to_graphs(batch, dataset, part, dtype=dtype)
+        targets = P.batch_targets(batch, dataset, params, comm, part, 0.9).astype(dtype)
+        losses, g0 = [], None
+        for it in range(tau):
+            loss, grads = P.loss_and_gradients(state, z["actions"], targets, params, comm)
+            g0 = g0 or grads
+            P.adam_step(params, grads, adam)
+            losses.append(loss)
+        return targets, losses, g0, adam
+    targets, losses, g0, adam = P.run_workers(1, worker)[0]
+    # targets come from the bit-exact forward: identical
+    assert np.array_equal(targets, z["targets"])
+    assert scale_error(losses, z["losses"]).max() < tol
+    for k in P.PARAM_NAMES:
+        assert scale_error(g0[k], z[f"g0_{k}"]).max() < tol, k
+        assert scale_error(getattr(params, k), z[f"p1_{k}"]).max() < tol, k
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.float32, 1e-4), (np.float64, 1e-9)])
+@pytest.mark.parametrize("K,L,B", [(8, 2, 3), (32, 3, 2), (64, 5, 4)])
+def test_loss_and_gradients_vs_port(dtype, tol, K, L, B):
+    rng = np.random.default_rng(K * 10 + L)
+    n = 400
+    graphs = [P.generate_ba(n, 3, 50 + i) for i in range(B)]
+    sols = (rng.random((B, n)) < 0.15).astype(np.uint8)
+    params = P.PolicyParams.initialize(K, L, seed=K, dtype=dtype, orientation="symmetric")
+    ps = port.ResidualState([g.edge_array for g in graphs], n, solutions=sols, dtype=dtype)
+    actions = np.array([int(np.flatnonzero(ps.cand[b])[rng.integers(
+        np.count_nonzero(ps.cand[b]))]) for b in range(B)])
+    targets = rng.normal(size=B).astype(dtype)
+
+    def worker(comm):
+        st = P.PartitionedState(graphs, P.partition_rows(n, 1)[0], solutions=sols, dtype=dtype)
+        return P.loss_and_gradients(st, actions, targets, params, comm)
+    loss, grads = P.run_workers(1, worker)[0]
+    loss_o, grads_o = port.loss_and_grads(ps, actions, targets, params.as_dict(), L)
+    assert abs(loss - loss_o) <= tol * max(1.0, abs(loss_o))
+    for k in P.PARAM_NAMES:
+        assert scale_error(grads[k], grads_o[k]).max() < tol, k
+
+
+def test_adam_bitwise_vs_port():
+    params = P.PolicyParams.initialize(16, 2, seed=3)
+    rng = np.random.default_rng(1)
+    theta = {k: v.copy() for k, v in params.as_dict().items()}
+    m = {k: np.zeros_like(v) for k, v in theta.items()}
+    v = {k: np.zeros_like(x) for k, x in theta.items()}
+    adam = P.AdamState.create(params, lr=1e-3)
+    step = 0
+
+    def run(grads):
+        return P.run_workers(1, lambda comm: P.adam_step(params, grads, adam))[0]
+    for it in range(3):
+        grads = {k: (rng.normal(size=x.shape) * 10.0 ** rng.integers(-3, 8)).astype(np.float32)
+                 for k, x in theta.items()}
+        run(grads)
+        step = port.adam(theta, grads, m, v, step, 1e-3)
+    for k in P.PARAM_NAMES:
+        assert np.array_equal(getattr(params, k), theta[k]), k
+        assert np.array_equal(adam.m[k], m[k]) and np.array_equal(adam.v[k], v[k])
