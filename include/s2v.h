@@ -68,6 +68,8 @@ typedef struct {
   uint8_t *sol;            /* [B*num_rows] partial solution S               */
   uint8_t *cand;           /* [B*num_rows] candidate set C                  */
   int64_t *residual;       /* [B] alive local entries                       */
+  const int32_t *order;    /* [B*num_rows] processing order (descending
+                              degree) for load balance; NULL = identity    */
 } s2v_shard;
 
 /* ---- library ------------------------------------------------------------ */

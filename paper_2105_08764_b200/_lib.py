@@ -40,6 +40,7 @@ class s2v_shard(ctypes.Structure):
         ("sol", ctypes.c_void_p),
         ("cand", ctypes.c_void_p),
         ("residual", ctypes.c_void_p),
+        ("order", ctypes.c_void_p),
     ]
 
 
@@ -127,7 +128,7 @@ def check(rc: int, what: str = "") -> None:
 
 # kernels each entry point launches (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {
-    "s2v_shard_init": 1, "s2v_apply_phase1": 1, "s2v_apply_phase2": 1, "s2v_e12_table": 1,
+    "s2v_shard_init": 1, "s2v_apply_phase1": 1, "s2v_apply_phase2": 2, "s2v_e12_table": 1,
     "s2v_embed_round": 1, "s2v_colsum": 2, "s2v_score": 1, "s2v_topk_merge": 1,
     "s2v_grad_h_init": 1, "s2v_layer_backward": 1, "s2v_gather": 1, "s2v_param_grads": 1,
     "s2v_reduce_partials": 1, "s2v_head_backward": 1, "s2v_adam": 1,

@@ -12,6 +12,8 @@
 // (SURVEY.md 3.4): sequential neighbour sums in ascending id, sequential FMA
 // chains for the theta projections, numpy pairwise sums, mul-then-add for the
 // theta7 contraction.  The library is compiled with -fmad=false.
+#include <algorithm>
+#include <array>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -27,6 +29,13 @@ template <class T>
 __global__ void e12_table_kernel(const T *__restrict__ t1, const T *__restrict__ t2,
                                  const T *__restrict__ t3, int K, int max_deg,
                                  T *__restrict__ table) {
+  extern __shared__ unsigned char smem_raw[];
+  T *th3T = reinterpret_cast<T *>(smem_raw);  // [K][K+1]: th3T[p][k] = theta3[k][p]
+  T *th2 = th3T + K * (K + 1);                // [K]
+  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x)
+    th3T[(idx % K) * (K + 1) + idx / K] = t3[idx];
+  for (int p = threadIdx.x; p < K; p += blockDim.x) th2[p] = t2[p];
+  __syncthreads();
   const int64_t total = (int64_t)(max_deg + 2) * K;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -34,7 +43,7 @@ __global__ void e12_table_kernel(const T *__restrict__ t1, const T *__restrict__
     const bool in_sol = row == max_deg + 1;
     const T deg = in_sol ? T(0) : T(row);
     T acc = T(0);
-    for (int p = 0; p < K; p++) acc = fmaT(t3[k * K + p], relu(mulT(t2[p], deg)), acc);
+    for (int p = 0; p < K; p++) acc = fmaT(th3T[p * (K + 1) + k], relu(mulT(th2[p], deg)), acc);
     const T e1 = mulT(t1[k], in_sol ? T(1) : T(0));
     table[idx] = addT(e1, acc);
   }
@@ -101,19 +110,51 @@ __global__ void __launch_bounds__(256) round_generic_kernel(
 // ---------------------------------------------------------------------------
 // Embedding round, K = 64 fp32 fast path.
 //
-// CTA = 256 threads processes tiles of 32 consecutive local rows.
-//  gather : 16 half-warps, each owns 2 rows; lane l of a half-warp holds
-//           m[4l..4l+3] (one float4 of the 256-byte neighbour row) and walks
-//           the row's neighbours in ascending order with 4 rows in flight.
+// CTA = 256 threads processes tiles of 32 local rows taken in descending
+// degree order (sh.order) from a dynamic tile counter, so rows of a tile have
+// similar neighbour counts and hub tiles start first.
+//  gather : 16 half-warps, each owns 2 rows of the tile; lane l of a
+//           half-warp holds m[4l..4l+3] (one float4 of the 256-byte neighbour
+//           row).  Neighbour ids are fetched 16 at a time (one per lane,
+//           coalesced) and broadcast with shuffles; rows are loaded in
+//           batches of 8 (all loads issued before the ascending-order adds).
+//           Rows of low physical id (BA hubs: most gathers) are loaded with
+//           an L2 evict_last policy, the rest evict_first.
 //  project: m tile [32][64] and theta4^T [64][64] in shared memory; each
-//           thread produces 2 rows x 4 k (float4 store), FMA chain p=0..63.
-// Rows of the tile are taken from a dynamic tile counter so that hub tiles
-// (low ids in BA graphs) start first and never hold up the tail.
+//           thread produces 2 rows x 4 k (float4 store), FMA chain p=0..63,
+//           then z = e12[deg] + chain, relu.
 // ---------------------------------------------------------------------------
 constexpr int kTileRows = 32;
 
-__device__ __forceinline__ float4 ldg_f4(const float *p) {
-  return __ldg(reinterpret_cast<const float4 *>(p));
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ float4 ldg_f4_pol(const float *ptr, uint64_t pol) {
+  float4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(ptr), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ void stg_f4_pol(float *ptr, const float4 &v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t ldg_u32_pol(const uint32_t *ptr, uint64_t pol) {
+  uint32_t v;
+  asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
+  return v;
 }
 
 __device__ __forceinline__ void add4(float4 &a, const float4 &b) {
@@ -123,45 +164,56 @@ __device__ __forceinline__ void add4(float4 &a, const float4 &b) {
   a.w = __fadd_rn(a.w, b.w);
 }
 
-// Sequential alive-neighbour sum of one row; 16 lanes, float4 each.
-__device__ __forceinline__ float4 gather_row64(const int64_t e0, const int64_t e1,
+// Sequential alive-neighbour sum of one row by one half-warp (lanes `sub`
+// 0..15 of mask `hmask`), float4 per lane.
+__device__ __forceinline__ float4 gather_row64(int64_t e, const int64_t e1,
                                                const uint32_t *__restrict__ cols,
-                                               const float *__restrict__ h_in, int sub) {
+                                               const float *__restrict__ h_in, int sub,
+                                               unsigned hmask, int hbase, uint32_t hot_rows,
+                                               uint64_t pol_hot, uint64_t pol_cold) {
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  int64_t e = e0;
-  // 8 neighbours per step: indices loaded cooperatively, rows issued before
-  // any add so 8 x 256 B are in flight per half-warp.
-  for (; e + 8 <= e1; e += 8) {
-    uint32_t c[8];
+  for (; e < e1; e += 16) {
+    const int cnt = (e1 - e) < 16 ? (int)(e1 - e) : 16;
+    const uint32_t mine = sub < cnt ? ldg_u32_pol(cols + e + sub, pol_cold) : S2V_DEAD;
 #pragma unroll
-    for (int q = 0; q < 8; q++) c[q] = __ldg(cols + e + q);
-    float4 v[8];
+    for (int half = 0; half < 2; half++) {
+      if (half * 8 >= cnt) break;
+      uint32_t c[8];
 #pragma unroll
-    for (int q = 0; q < 8; q++)
-      v[q] = (c[q] & S2V_DEAD) ? make_float4(0.f, 0.f, 0.f, 0.f)
-                               : ldg_f4(h_in + (int64_t)c[q] * 64 + sub * 4);
+      for (int q = 0; q < 8; q++) c[q] = __shfl_sync(hmask, mine, hbase + half * 8 + q);
+      float4 v[8];
 #pragma unroll
-    for (int q = 0; q < 8; q++)
-      if (!(c[q] & S2V_DEAD)) add4(acc, v[q]);
-  }
-  for (; e < e1; e++) {
-    uint32_t c = __ldg(cols + e);
-    if (!(c & S2V_DEAD)) add4(acc, ldg_f4(h_in + (int64_t)c * 64 + sub * 4));
+      for (int q = 0; q < 8; q++) {
+        if (c[q] & S2V_DEAD) {
+          v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          const float *src = h_in + (int64_t)c[q] * 64 + sub * 4;
+          v[q] = ldg_f4_pol(src, c[q] < hot_rows ? pol_hot : pol_cold);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; q++)
+        if (!(c[q] & S2V_DEAD)) add4(acc, v[q]);
+    }
   }
   return acc;
 }
 
-__global__ void __launch_bounds__(256, 2) round64_kernel(
+__global__ void __launch_bounds__(256, 4) round64_kernel(
     s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ table, int max_deg,
     const float *__restrict__ h_in, float *__restrict__ h_out, float *__restrict__ m_out,
-    int *__restrict__ tile_counter) {
-  __shared__ __align__(16) float thT[64][64 + 4];           // thT[p][k] = theta4[k][p]
-  __shared__ __align__(16) float ms[kTileRows][64 + 4];     // m tile
+    int *__restrict__ tile_counter, uint32_t hot_rows) {
+  __shared__ __align__(16) float thT[64][64 + 4];        // thT[p][k] = theta4[k][p]
+  __shared__ __align__(16) float ms[kTileRows][64 + 4];  // m tile
+  __shared__ int32_t s_rows[kTileRows];
   __shared__ int s_tile;
   for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x)
     thT[idx % 64][idx / 64] = theta4[idx];
   const int tid = threadIdx.x;
   const int hw = tid >> 4, sub = tid & 15;  // half-warp id, lane in half-warp
+  const unsigned hmask = (tid & 16) ? 0xFFFF0000u : 0x0000FFFFu;
+  const int hbase = tid & 16;
+  const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
   const int64_t ntiles = (nrows + kTileRows - 1) / kTileRows;
   for (;;) {
@@ -170,17 +222,22 @@ __global__ void __launch_bounds__(256, 2) round64_kernel(
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
-    const int64_t r0 = tile * kTileRows;
+    if (tid < kTileRows) {
+      const int64_t q = tile * kTileRows + tid;
+      s_rows[tid] = q < nrows ? (sh.order ? sh.order[q] : (int32_t)q) : -1;
+    }
+    __syncthreads();
     // ---- gather: each half-warp handles rows hw and hw+16 of the tile
 #pragma unroll
     for (int q = 0; q < 2; q++) {
       const int lr = hw + 16 * q;
-      const int64_t r = r0 + lr;
+      const int64_t r = s_rows[lr];
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (h_in && r < nrows && !sh.sol[r])
-        acc = gather_row64(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, h_in, sub);
+      if (h_in && r >= 0 && !sh.sol[r])
+        acc = gather_row64(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, h_in, sub, hmask, hbase,
+                           hot_rows, pol_hot, pol_cold);
       *reinterpret_cast<float4 *>(&ms[lr][sub * 4]) = acc;
-      if (m_out && r < nrows) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
+      if (m_out && r >= 0) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
     }
     __syncthreads();
     // ---- projection: thread -> rows {rp, rp+16}, k in [4*kq, 4*kq+4)
@@ -205,8 +262,8 @@ __global__ void __launch_bounds__(256, 2) round64_kernel(
     }
 #pragma unroll
     for (int a = 0; a < 2; a++) {
-      const int64_t r = r0 + rp + 16 * a;
-      if (r >= nrows) continue;
+      const int64_t r = s_rows[rp + 16 * a];
+      if (r < 0) continue;
       const int64_t b = r / sh.num_rows, i = r - b * sh.num_rows;
       const int trow = sh.sol[r] ? max_deg + 1 : sh.rdeg[r];
       const float4 e = *reinterpret_cast<const float4 *>(table + (int64_t)trow * 64 + kq * 4);
@@ -216,19 +273,24 @@ __global__ void __launch_bounds__(256, 2) round64_kernel(
       o.z = relu(__fadd_rn(e.z, z[a][2]));
       o.w = relu(__fadd_rn(e.w, z[a][3]));
       const int64_t phys = (b * sh.world + sh.rank) * sh.rows_max + i;
-      *reinterpret_cast<float4 *>(h_out + phys * 64 + kq * 4) = o;
+      stg_f4_pol(h_out + phys * 64 + kq * 4, o, pol_cold);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// numpy pairwise column sums over the N nodes of each slot.
-// Plan (host, cached per N): "roots" = maximal subtrees of numpy's recursion
-// with <= kRootMax elements, plus the post-order program of the tree above
-// them.  Leaf kernel: one CTA per (root, slot), one thread per k.
+// numpy pairwise column sums over the N nodes of each slot (policy.py:199).
+//
+// numpy's pairwise_sum(a, n): n < 8 sequential; n <= 128 eight strided
+// accumulators r[j] (r[j] = a[j] + a[j+8] + ... sequentially) combined as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then a sequential tail; else split at
+// n2 = n/2 - (n/2)%8 and return left + right.  The recursion tree depends on
+// N only, so the host enumerates it once per N (cached): leaves in order and
+// internal nodes grouped by height.  Then
+//   leaf kernel : one thread per (leaf, k, j) runs accumulator chain r[j]
+//                 (16 independent loads in flight), j = 0 combines + tail;
+//   level kernel: one launch per height, vals[node] = vals[left] + vals[right].
 // ---------------------------------------------------------------------------
-constexpr int64_t kRootMax = 1024;
-
 struct PairwiseCtx {
   const void *h;
   int64_t N, rows_max, base, extra;
@@ -237,133 +299,99 @@ struct PairwiseCtx {
 
 template <class T>
 __device__ __forceinline__ T load_node(const PairwiseCtx &c, int64_t u, int k) {
-  const int64_t big = c.extra * (c.base + 1);
-  const int64_t r = u < big ? u / (c.base + 1) : c.extra + (u - big) / c.base;
-  const int64_t start = r * c.base + (r < c.extra ? r : c.extra);
-  const int64_t phys = ((int64_t)c.b * c.P + r) * c.rows_max + (u - start);
+  int64_t phys;
+  if (c.P == 1) {
+    phys = (int64_t)c.b * c.rows_max + u;
+  } else {
+    const int64_t big = c.extra * (c.base + 1);
+    const int64_t r = u < big ? u / (c.base + 1) : c.extra + (u - big) / c.base;
+    const int64_t start = r * c.base + (r < c.extra ? r : c.extra);
+    phys = ((int64_t)c.b * c.P + r) * c.rows_max + (u - start);
+  }
   return reinterpret_cast<const T *>(c.h)[phys * c.K + k];
 }
 
-// numpy pairwise_sum leaf (n <= 128): 8 strided accumulators + sequential tail.
+// grid (nleaves, ceil(K/32), B), block (32 k, 8 j)
 template <class T>
-__device__ __forceinline__ T pairwise_leaf(const PairwiseCtx &c, int64_t u0, int64_t n, int k) {
-  if (n < 8) {
-    T res = T(0);
-    for (int64_t i = 0; i < n; i++) res = addT(res, load_node<T>(c, u0 + i, k));
-    return res;
+__global__ void __launch_bounds__(256) colsum_leaf_kernel(PairwiseCtx c,
+                                                          const int64_t *__restrict__ leaves,
+                                                          int64_t nvals, T *__restrict__ vals) {
+  __shared__ T part[8][32];
+  c.b = blockIdx.z;
+  const int leaf = blockIdx.x;
+  const int kl = threadIdx.x, j = threadIdx.y;
+  const int k = blockIdx.y * 32 + kl;
+  const int64_t u0 = leaves[2 * leaf], n = leaves[2 * leaf + 1];
+  const bool ok = k < c.K;
+  if (n >= 8 && ok) {
+    const int64_t stop = n - (n % 8);
+    T r = load_node<T>(c, u0 + j, k);
+    for (int64_t i = 8 + j; i < stop; i += 8) r = addT(r, load_node<T>(c, u0 + i, k));
+    part[j][kl] = r;
   }
-  T r[8];
-#pragma unroll
-  for (int j = 0; j < 8; j++) r[j] = load_node<T>(c, u0 + j, k);
-  int64_t i;
-  for (i = 8; i < n - (n % 8); i += 8) {
-#pragma unroll
-    for (int j = 0; j < 8; j++) r[j] = addT(r[j], load_node<T>(c, u0 + i + j, k));
-  }
-  T res = addT(addT(addT(r[0], r[1]), addT(r[2], r[3])), addT(addT(r[4], r[5]), addT(r[6], r[7])));
-  for (; i < n; i++) res = addT(res, load_node<T>(c, u0 + i, k));
-  return res;
-}
-
-// numpy pairwise_sum of n elements, recursion unrolled onto an explicit stack
-// (split n2 = n/2 - (n/2)%8, left + right).
-template <class T>
-__device__ T pairwise_dev(const PairwiseCtx &c, int64_t u0, int64_t n, int k) {
-  struct Frame {
-    int64_t u0, n;
-    int stage;
-    T left;
-  };
-  Frame st[24];
-  int sp = 0;
-  st[0].u0 = u0;
-  st[0].n = n;
-  st[0].stage = 0;
-  T ret = T(0);
-  for (;;) {
-    Frame &f = st[sp];
-    if (f.n <= 128) {
-      ret = pairwise_leaf<T>(c, f.u0, f.n, k);
-      if (sp == 0) return ret;
-      sp--;
-      continue;
-    }
-    int64_t n2 = f.n / 2;
-    n2 -= n2 % 8;
-    if (f.stage == 0) {
-      f.stage = 1;
-      Frame &ch = st[++sp];
-      ch.u0 = f.u0;
-      ch.n = n2;
-      ch.stage = 0;
-    } else if (f.stage == 1) {
-      f.left = ret;
-      f.stage = 2;
-      Frame &ch = st[++sp];
-      ch.u0 = f.u0 + n2;
-      ch.n = f.n - n2;
-      ch.stage = 0;
+  __syncthreads();
+  if (j == 0 && ok) {
+    T res;
+    int64_t i;
+    if (n < 8) {
+      res = T(0);
+      i = 0;
     } else {
-      ret = addT(f.left, ret);
-      if (sp == 0) return ret;
-      sp--;
+      res = addT(addT(addT(part[0][kl], part[1][kl]), addT(part[2][kl], part[3][kl])),
+                 addT(addT(part[4][kl], part[5][kl]), addT(part[6][kl], part[7][kl])));
+      i = n - (n % 8);
     }
+    for (; i < n; i++) res = addT(res, load_node<T>(c, u0 + i, k));
+    vals[((int64_t)c.b * nvals + leaf) * c.K + k] = res;
+  }
+}
+
+// vals[b][base + q] = vals[b][left[q]] + vals[b][right[q]] for q in [0, count)
+template <class T>
+__global__ void colsum_level_kernel(const int32_t *__restrict__ left,
+                                    const int32_t *__restrict__ right, int count, int base,
+                                    int64_t nvals, int K, T *__restrict__ vals) {
+  const int b = blockIdx.y;
+  T *v = vals + (int64_t)b * nvals * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)count * K;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(e / K), k = (int)(e - (int64_t)q * K);
+    v[(int64_t)(base + q) * K + k] = addT(v[(int64_t)left[q] * K + k], v[(int64_t)right[q] * K + k]);
   }
 }
 
 template <class T>
-__global__ void colsum_roots_kernel(PairwiseCtx c, const int64_t *__restrict__ roots,
-                                    int nroots, T *__restrict__ root_sums) {
-  c.b = blockIdx.y;
-  const int root = blockIdx.x;
-  for (int k = threadIdx.x; k < c.K; k += blockDim.x) {
-    T v = pairwise_dev<T>(c, roots[2 * root], roots[2 * root + 1], k);
-    root_sums[((int64_t)c.b * nroots + root) * c.K + k] = v;
-  }
-}
-
-// prog: post-order over roots; entry >= 0 pushes root_sums[entry], -1 pops
-// right then left and pushes left + right.
-template <class T>
-__global__ void colsum_top_kernel(const int32_t *__restrict__ prog, int nprog, int nroots,
-                                  int K, const T *__restrict__ root_sums, T *__restrict__ g) {
+__global__ void colsum_out_kernel(int root, int64_t nvals, int K, const T *__restrict__ vals,
+                                  T *__restrict__ g) {
   const int b = blockIdx.x;
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    T stack[48];
-    int sp = 0;
-    for (int i = 0; i < nprog; i++) {
-      int op = prog[i];
-      if (op >= 0) {
-        stack[sp++] = root_sums[((int64_t)b * nroots + op) * K + k];
-      } else {
-        T rgt = stack[--sp];
-        T lft = stack[--sp];
-        stack[sp++] = addT(lft, rgt);
-      }
-    }
-    g[(int64_t)b * K + k] = addT(T(0), stack[0]);
-  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x)
+    g[(int64_t)b * K + k] = addT(T(0), vals[((int64_t)b * nvals + root) * K + k]);
 }
 
 struct PairwisePlan {
-  int64_t *d_roots = nullptr;  // [nroots][2] (start, len)
-  int32_t *d_prog = nullptr;
-  int nroots = 0, nprog = 0;
+  int64_t *d_leaves = nullptr;  // [nleaves][2] (start, len)
+  int32_t *d_left = nullptr, *d_right = nullptr;  // internal nodes, by height
+  int nleaves = 0, ninternal = 0, root = 0;
+  std::vector<int> level_start;  // internal index ranges per height
 };
 
-static void build_plan(int64_t u0, int64_t n, std::vector<int64_t> &roots,
-                       std::vector<int32_t> &prog) {
-  if (n <= kRootMax) {
-    prog.push_back((int32_t)(roots.size() / 2));
-    roots.push_back(u0);
-    roots.push_back(n);
-    return;
+// returns (node id, height); ids < nleaves are leaves, internal nodes get
+// provisional ids in creation order and are renumbered by height afterwards
+static std::pair<int, int> plan_rec(int64_t u0, int64_t n, std::vector<int64_t> &leaves,
+                                    std::vector<std::array<int, 3>> &internal) {
+  if (n <= 128) {
+    leaves.push_back(u0);
+    leaves.push_back(n);
+    return {(int)(leaves.size() / 2 - 1), 0};
   }
   int64_t n2 = n / 2;
   n2 -= n2 % 8;
-  build_plan(u0, n2, roots, prog);
-  build_plan(u0 + n2, n - n2, roots, prog);
-  prog.push_back(-1);
+  auto l = plan_rec(u0, n2, leaves, internal);
+  auto r = plan_rec(u0 + n2, n - n2, leaves, internal);
+  int h = std::max(l.second, r.second) + 1;
+  internal.push_back({l.first | (l.second ? (1 << 30) : 0), r.first | (r.second ? (1 << 30) : 0),
+                      h});
+  return {(int)internal.size() - 1, h};
 }
 
 static int get_plan(int64_t N, PairwisePlan **out) {
@@ -375,21 +403,83 @@ static int get_plan(int64_t N, PairwisePlan **out) {
   auto key = std::make_pair(dev, N);
   auto it = cache.find(key);
   if (it == cache.end()) {
-    std::vector<int64_t> roots;
-    std::vector<int32_t> prog;
-    build_plan(0, N, roots, prog);
+    std::vector<int64_t> leaves;
+    std::vector<std::array<int, 3>> internal;  // {left, right, height}; bit 30 = internal
+    auto rootp = plan_rec(0, N, leaves, internal);
     PairwisePlan p;
-    p.nroots = (int)(roots.size() / 2);
-    p.nprog = (int)prog.size();
-    S2V_CUDA_CHECK(cudaMalloc(&p.d_roots, sizeof(int64_t) * roots.size()));
-    S2V_CUDA_CHECK(cudaMalloc(&p.d_prog, sizeof(int32_t) * prog.size()));
-    S2V_CUDA_CHECK(cudaMemcpy(p.d_roots, roots.data(), sizeof(int64_t) * roots.size(),
+    p.nleaves = (int)(leaves.size() / 2);
+    p.ninternal = (int)internal.size();
+    // renumber internal nodes by height (stable): id = nleaves + rank
+    std::vector<int> order(internal.size());
+    for (size_t q = 0; q < order.size(); q++) order[q] = (int)q;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return internal[a][2] < internal[b][2]; });
+    std::vector<int> newid(internal.size());
+    for (size_t q = 0; q < order.size(); q++) newid[order[q]] = p.nleaves + (int)q;
+    auto resolve = [&](int x) { return (x & (1 << 30)) ? newid[x & ~(1 << 30)] : x; };
+    std::vector<int32_t> left(internal.size()), right(internal.size());
+    int cur_h = -1;
+    for (size_t q = 0; q < order.size(); q++) {
+      const auto &nd = internal[order[q]];
+      left[q] = resolve(nd[0]);
+      right[q] = resolve(nd[1]);
+      if (nd[2] != cur_h) {
+        p.level_start.push_back((int)q);
+        cur_h = nd[2];
+      }
+    }
+    p.level_start.push_back((int)internal.size());
+    p.root = rootp.second ? newid[rootp.first] : rootp.first;
+    S2V_CUDA_CHECK(cudaMalloc(&p.d_leaves, sizeof(int64_t) * leaves.size()));
+    S2V_CUDA_CHECK(cudaMemcpy(p.d_leaves, leaves.data(), sizeof(int64_t) * leaves.size(),
                               cudaMemcpyHostToDevice));
-    S2V_CUDA_CHECK(cudaMemcpy(p.d_prog, prog.data(), sizeof(int32_t) * prog.size(),
-                              cudaMemcpyHostToDevice));
-    it = cache.emplace(key, p).first;
+    if (!internal.empty()) {
+      S2V_CUDA_CHECK(cudaMalloc(&p.d_left, sizeof(int32_t) * left.size()));
+      S2V_CUDA_CHECK(cudaMalloc(&p.d_right, sizeof(int32_t) * right.size()));
+      S2V_CUDA_CHECK(cudaMemcpy(p.d_left, left.data(), sizeof(int32_t) * left.size(),
+                                cudaMemcpyHostToDevice));
+      S2V_CUDA_CHECK(cudaMemcpy(p.d_right, right.data(), sizeof(int32_t) * right.size(),
+                                cudaMemcpyHostToDevice));
+    }
+    it = cache.emplace(key, std::move(p)).first;
   }
   *out = &it->second;
+  return S2V_OK;
+}
+
+template <class T>
+static int colsum_t(const s2v_shard *sh, int K, const void *h, void *g, void *workspace,
+                    size_t workspace_bytes, cudaStream_t st) {
+  PairwisePlan *plan = nullptr;
+  int rc = get_plan(sh->num_nodes, &plan);
+  if (rc) return rc;
+  const int64_t nvals = (int64_t)plan->nleaves + plan->ninternal;
+  if (workspace_bytes < (size_t)nvals * sh->batch * K * sizeof(T))
+    return fail(S2V_EINVAL, "colsum workspace too small");
+  T *vals = (T *)workspace;
+  PairwiseCtx c;
+  c.h = h;
+  c.N = sh->num_nodes;
+  c.rows_max = sh->rows_max;
+  c.P = sh->world;
+  c.base = sh->num_nodes / sh->world;
+  c.extra = sh->num_nodes % sh->world;
+  c.K = K;
+  c.b = 0;
+  dim3 lgrid(plan->nleaves, (K + 31) / 32, sh->batch);
+  colsum_leaf_kernel<T><<<lgrid, dim3(32, 8), 0, st>>>(c, plan->d_leaves, nvals, vals);
+  S2V_LAUNCH_CHECK();
+  for (size_t lv = 0; lv + 1 < plan->level_start.size(); lv++) {
+    const int a = plan->level_start[lv], bnd = plan->level_start[lv + 1];
+    const int count = bnd - a;
+    int64_t work = (int64_t)count * K;
+    int blocks = (int)std::min<int64_t>((work + 255) / 256, kNumSMs * 8);
+    colsum_level_kernel<T><<<dim3(blocks, sh->batch), 256, 0, st>>>(
+        plan->d_left + a, plan->d_right + a, count, plan->nleaves + a, nvals, K, vals);
+    S2V_LAUNCH_CHECK();
+  }
+  colsum_out_kernel<T><<<sh->batch, 64, 0, st>>>(plan->root, nvals, K, vals, (T *)g);
+  S2V_LAUNCH_CHECK();
   return S2V_OK;
 }
 
@@ -397,7 +487,7 @@ static int get_plan(int64_t N, PairwisePlan **out) {
 // Scores + selection keys, generic: one warp per local row.
 // ---------------------------------------------------------------------------
 constexpr int kTopK = 8;
-constexpr int kScoreRowsPerBlock = 256;
+constexpr int kScoreRowsPerBlock = 2048;
 
 __device__ __forceinline__ void insert_top(Key (&top)[kTopK], const Key &k) {
   if (!key_gt(k, top[kTopK - 1])) return;
@@ -409,14 +499,16 @@ __device__ __forceinline__ void insert_top(Key (&top)[kTopK], const Key &k) {
   top[pos] = k;
 }
 
-// Block-wide merge of per-thread top lists held by lane 0 of each warp... kept
-// simple: every thread owns a list; lists are merged through shared memory.
-__device__ void block_merge_top(Key (&top)[kTopK], Key *s_keys /*[blockDim*8]*/,
-                                Key *out) {
+// Merge the per-thread top lists of threads [0, n) (n a power of two, all
+// threads of the block call this) through shared memory into out[0..8).
+__device__ void block_merge_top(Key (&top)[kTopK], Key *s_keys /*[n*8]*/, Key *out,
+                                int n = -1) {
   const int tid = threadIdx.x;
-  for (int q = 0; q < kTopK; q++) s_keys[tid * kTopK + q] = top[q];
+  if (n < 0) n = blockDim.x;
+  if (tid < n)
+    for (int q = 0; q < kTopK; q++) s_keys[tid * kTopK + q] = top[q];
   __syncthreads();
-  for (int stride = blockDim.x / 2; stride > 0; stride >>= 1) {
+  for (int stride = n / 2; stride > 0; stride >>= 1) {
     if (tid < stride) {
       for (int q = 0; q < kTopK; q++) insert_top(top, s_keys[(tid + stride) * kTopK + q]);
       for (int q = 0; q < kTopK; q++) s_keys[tid * kTopK + q] = top[q];
@@ -487,6 +579,112 @@ __global__ void __launch_bounds__(256) score_generic_kernel(
     atomicAdd((unsigned long long *)&counts[b], s_count);
 }
 
+// K = 64 fp32 scorer: tiles of 64 rows; u2 = theta6 (h*cand) as a 4x4
+// register-tiled FMA chain (p = 0..63 per output), then one thread per row
+// runs the sequential theta7 contraction (mul then add, j = 0..127).
+constexpr int kScoreTile = 64;
+
+__global__ void __launch_bounds__(256, 3) score64_kernel(
+    s2v_shard sh, const float *__restrict__ h, const float *__restrict__ u1,
+    const float *__restrict__ theta6, const float *__restrict__ theta7,
+    const uint8_t *__restrict__ cand_override, int mode, float *__restrict__ scores,
+    Key *__restrict__ block_keys, int64_t *__restrict__ counts) {
+  __shared__ __align__(16) float th6T[64][68];           // th6T[p][k] = theta6[k][p]
+  // xs[row][p] = h[row][p]*c; after the projection the same storage holds
+  // prod[row][k] = fl(relu(u2) * theta7), and at the end the key lists
+  __shared__ __align__(16) float xbuf[kScoreTile * 68];
+  float(*xs)[68] = reinterpret_cast<float(*)[68]>(xbuf);
+  float(*prod)[65] = reinterpret_cast<float(*)[65]>(xbuf);
+  __shared__ float s_t7[64];
+  __shared__ uint8_t s_c[kScoreTile];
+  __shared__ float s_s0;
+  __shared__ unsigned long long s_count;
+  Key *s_keys = reinterpret_cast<Key *>(xbuf);
+  const int b = blockIdx.y, tid = threadIdx.x;
+  for (int idx = tid; idx < 64 * 64; idx += 256) th6T[idx % 64][idx / 64] = theta6[idx];
+  if (tid < 64) s_t7[tid] = theta7[64 + tid];
+  if (tid == 0) {
+    float s0 = 0.f;
+    for (int j = 0; j < 64; j++) s0 = __fadd_rn(s0, __fmul_rn(relu(u1[b * 64 + j]), theta7[j]));
+    s_s0 = s0;
+    s_count = 0;
+  }
+  Key top[kTopK];
+#pragma unroll
+  for (int q = 0; q < kTopK; q++) top[q] = null_key();
+  unsigned long long cnt = 0;
+  const int64_t i0 = (int64_t)blockIdx.x * kScoreRowsPerBlock;
+  const int64_t i1 = min(i0 + kScoreRowsPerBlock, sh.num_rows);
+  const int64_t base_r = (int64_t)b * sh.num_rows;
+  const int64_t base_phys = ((int64_t)b * sh.world + sh.rank) * sh.rows_max;
+  const int kq = tid & 15, rq = tid >> 4;
+  for (int64_t t0 = i0; t0 < i1; t0 += kScoreTile) {
+    __syncthreads();
+    // load x = h * cand (fl(h*1) = h, fl(h*0) = +-0)
+    for (int e = tid; e < kScoreTile * 16; e += 256) {
+      const int row = e >> 4, k4 = e & 15;
+      const int64_t i = t0 + row;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      float c = 0.f;
+      if (i < i1) {
+        const uint8_t cb = cand_override ? cand_override[base_r + i] : sh.cand[base_r + i];
+        c = cb ? 1.f : 0.f;
+        if (k4 == 0) s_c[row] = cb;
+        v = *reinterpret_cast<const float4 *>(h + (base_phys + i) * 64 + k4 * 4);
+      } else if (k4 == 0) {
+        s_c[row] = 0;
+      }
+      float4 x;
+      x.x = __fmul_rn(v.x, c);
+      x.y = __fmul_rn(v.y, c);
+      x.z = __fmul_rn(v.z, c);
+      x.w = __fmul_rn(v.w, c);
+      *reinterpret_cast<float4 *>(&xs[row][k4 * 4]) = x;
+    }
+    __syncthreads();
+    float acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int c = 0; c < 4; c++) acc[a][c] = 0.f;
+#pragma unroll 4
+    for (int p = 0; p < 64; p++) {
+      const float4 t = *reinterpret_cast<const float4 *>(&th6T[p][kq * 4]);
+#pragma unroll
+      for (int a = 0; a < 4; a++) {
+        const float xr = xs[rq * 4 + a][p];
+        acc[a][0] = __fmaf_rn(t.x, xr, acc[a][0]);
+        acc[a][1] = __fmaf_rn(t.y, xr, acc[a][1]);
+        acc[a][2] = __fmaf_rn(t.z, xr, acc[a][2]);
+        acc[a][3] = __fmaf_rn(t.w, xr, acc[a][3]);
+      }
+    }
+    __syncthreads();  // xT fully consumed before prod overwrites it
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int c = 0; c < 4; c++)
+        prod[rq * 4 + a][kq * 4 + c] = __fmul_rn(relu(acc[a][c]), s_t7[kq * 4 + c]);
+    __syncthreads();
+    if (tid < kScoreTile && t0 + tid < i1) {
+      float sc = s_s0;
+#pragma unroll 16
+      for (int k = 0; k < 64; k++) sc = __fadd_rn(sc, prod[tid][k]);
+      const int64_t i = t0 + tid;
+      scores[base_r + i] = sc;
+      const bool c = s_c[tid] != 0;
+      const bool finite = isfinite(sc);
+      if (c && finite) cnt++;
+      if (c && (finite || mode == 1)) insert_top(top, make_key((double)sc, sh.row_start + i));
+    }
+  }
+  if (cnt) atomicAdd(&s_count, cnt);
+  __syncthreads();  // prod fully consumed before the key lists reuse it
+  block_merge_top(top, s_keys, block_keys + ((int64_t)b * gridDim.x + blockIdx.x) * kTopK,
+                  kScoreTile);
+  if (tid == 0 && s_count) atomicAdd((unsigned long long *)&counts[b], s_count);
+}
+
 __global__ void topk_merge_kernel(const Key *__restrict__ block_keys, int nblk, int d,
                                   Key *__restrict__ top_out) {
   extern __shared__ unsigned char smem_raw[];
@@ -495,8 +693,18 @@ __global__ void topk_merge_kernel(const Key *__restrict__ block_keys, int nblk, 
   Key top[kTopK];
 #pragma unroll
   for (int q = 0; q < kTopK; q++) top[q] = null_key();
-  for (int64_t idx = threadIdx.x; idx < (int64_t)nblk * kTopK; idx += blockDim.x)
-    insert_top(top, block_keys[(int64_t)b * nblk * kTopK + idx]);
+  const Key *src = block_keys + (int64_t)b * nblk * kTopK;
+  const int64_t total = (int64_t)nblk * kTopK;
+  int64_t idx = threadIdx.x;
+  for (; idx + 3 * blockDim.x < total; idx += 4 * blockDim.x) {
+    Key k0 = src[idx], k1 = src[idx + blockDim.x], k2 = src[idx + 2 * blockDim.x],
+        k3 = src[idx + 3 * blockDim.x];
+    insert_top(top, k0);
+    insert_top(top, k1);
+    insert_top(top, k2);
+    insert_top(top, k3);
+  }
+  for (; idx < total; idx += blockDim.x) insert_top(top, src[idx]);
   __shared__ Key s_out[kTopK];
   block_merge_top(top, s_keys, s_out);
   __syncthreads();
@@ -514,10 +722,19 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
     if (!counter) S2V_CUDA_CHECK(cudaMalloc(&counter, sizeof(int)));
     S2V_CUDA_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), st));
     int64_t ntiles = (nrows + kTileRows - 1) / kTileRows;
-    int grid = (int)std::min<int64_t>(ntiles, kNumSMs * 2);
+    int grid = (int)std::min<int64_t>(ntiles, kNumSMs * 4);
+    // rows kept in L2 with evict_last: the lowest physical ids -- the BA hubs,
+    // 48 MB of rows source 31% of all gathers at BA(2M,16) (measured best of
+    // 0/48/80/110 MB; S2V_HOT_MB overrides)
+    uint32_t hot_rows;
+    static const uint32_t hot_env = [] {
+      const char *e = getenv("S2V_HOT_MB");
+      return (uint32_t)(e ? atoi(e) : 48);
+    }();
+    hot_rows = (uint32_t)(((uint64_t)hot_env << 20) / 256);
     round64_kernel<<<grid, 256, 0, st>>>(*sh, (const float *)theta4, (const float *)table,
                                          max_deg, (const float *)h_in, (float *)h_out,
-                                         (float *)m_out, counter);
+                                         (float *)m_out, counter, hot_rows);
     S2V_LAUNCH_CHECK();
     return S2V_OK;
   }
@@ -556,14 +773,22 @@ int s2v_e12_table(s2v_dtype dt, const void *theta1, const void *theta2, const vo
   if (K < 1 || max_deg < 0) return fail(S2V_EINVAL, "bad e12 table args");
   int64_t total = (int64_t)(max_deg + 2) * K;
   int grid = (int)std::min<int64_t>((total + 255) / 256, kNumSMs * 8);
-  if (dt == S2V_F32)
-    e12_table_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(
+  if (K > 256) return fail(S2V_EINVAL, "embed_dim %d > 256 unsupported", K);
+  size_t elem = dt == S2V_F32 ? 4 : 8;
+  size_t smem = elem * ((size_t)K * (K + 1) + K);
+  if (dt == S2V_F32) {
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(e12_table_kernel<float>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    e12_table_kernel<float><<<grid, 256, smem, as_stream(stream)>>>(
         (const float *)theta1, (const float *)theta2, (const float *)theta3, K, max_deg,
         (float *)table);
-  else
-    e12_table_kernel<double><<<grid, 256, 0, as_stream(stream)>>>(
+  } else {
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(e12_table_kernel<double>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    e12_table_kernel<double><<<grid, 256, smem, as_stream(stream)>>>(
         (const double *)theta1, (const double *)theta2, (const double *)theta3, K, max_deg,
         (double *)table);
+  }
   S2V_LAUNCH_CHECK();
   return S2V_OK;
 }
@@ -578,43 +803,16 @@ int s2v_embed_round(s2v_dtype dt, const s2v_shard *sh, const void *theta4, const
 }
 
 size_t s2v_colsum_workspace(const s2v_shard *sh, int K, int elem_bytes) {
-  // upper bound on roots: ceil(N / (kRootMax/2)) + 1
-  int64_t nroots = sh->num_nodes / (kRootMax / 2) + 2;
-  return (size_t)nroots * sh->batch * K * elem_bytes;
+  // leaves have > 56 elements unless N < 128; nodes = 2 * leaves - 1
+  int64_t nleaves = sh->num_nodes / 56 + 2;
+  return (size_t)(2 * nleaves) * sh->batch * K * elem_bytes;
 }
 
 int s2v_colsum(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, void *g,
                void *workspace, size_t workspace_bytes, void *stream) {
-  PairwisePlan *plan = nullptr;
-  int rc = get_plan(sh->num_nodes, &plan);
-  if (rc) return rc;
-  size_t need = (size_t)plan->nroots * sh->batch * K * (dt == S2V_F32 ? 4 : 8);
-  if (workspace_bytes < need) return fail(S2V_EINVAL, "colsum workspace too small");
-  PairwiseCtx c;
-  c.h = h;
-  c.N = sh->num_nodes;
-  c.rows_max = sh->rows_max;
-  c.P = sh->world;
-  c.base = sh->num_nodes / sh->world;
-  c.extra = sh->num_nodes % sh->world;
-  c.K = K;
-  c.b = 0;
-  cudaStream_t st = as_stream(stream);
-  dim3 grid(plan->nroots, sh->batch);
-  int threads = K < 32 ? 32 : (K > 256 ? 256 : K);
-  if (dt == S2V_F32) {
-    colsum_roots_kernel<float><<<grid, threads, 0, st>>>(c, plan->d_roots, plan->nroots,
-                                                         (float *)workspace);
-    colsum_top_kernel<float><<<sh->batch, threads, 0, st>>>(
-        plan->d_prog, plan->nprog, plan->nroots, K, (const float *)workspace, (float *)g);
-  } else {
-    colsum_roots_kernel<double><<<grid, threads, 0, st>>>(c, plan->d_roots, plan->nroots,
-                                                          (double *)workspace);
-    colsum_top_kernel<double><<<sh->batch, threads, 0, st>>>(
-        plan->d_prog, plan->nprog, plan->nroots, K, (const double *)workspace, (double *)g);
-  }
-  S2V_LAUNCH_CHECK();
-  return S2V_OK;
+  if (dt == S2V_F32)
+    return colsum_t<float>(sh, K, h, g, workspace, workspace_bytes, as_stream(stream));
+  return colsum_t<double>(sh, K, h, g, workspace, workspace_bytes, as_stream(stream));
 }
 
 int s2v_score_blocks(const s2v_shard *sh) {
@@ -631,7 +829,12 @@ int s2v_score(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, const voi
   dim3 grid(s2v_score_blocks(sh), sh->batch);
   size_t elem = dt == S2V_F32 ? 4 : 8;
   size_t smem = elem * ((size_t)K * (K + 1) + 16 * (size_t)K) + sizeof(Key) * 256 * kTopK;
-  if (dt == S2V_F32) {
+  if (dt == S2V_F32 && K == 64) {
+    score64_kernel<<<grid, 256, 0, st>>>(*sh, (const float *)h, (const float *)u1,
+                                         (const float *)theta6, (const float *)theta7,
+                                         cand_override, mode, (float *)scores, (Key *)block_keys,
+                                         counts);
+  } else if (dt == S2V_F32) {
     auto kern = score_generic_kernel<float>;
     S2V_CUDA_CHECK(
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

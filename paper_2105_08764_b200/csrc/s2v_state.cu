@@ -121,76 +121,102 @@ __global__ void apply_phase1_kernel(s2v_shard sh, PartitionMap pm, const int64_t
   }
 }
 
-// Phase 2 (every rank): replay the skip rule identically, then apply the
-// accepted picks to this rank's rows (row v if owned) and columns (entries
-// whose neighbour is v).  One CTA per slot; picks are applied in order.
+// Replay of the mid-group skip rule (inference.py:127-146) from phase-1
+// info: pick j > 0 stays a candidate iff rdeg(v_j) minus the number of
+// earlier accepted picks it shares an alive edge with is > 0.  Returns the
+// accepted mask and the global number of removed entries (2 * rdeg at apply).
+__device__ uint64_t replay_group(const int64_t *picks, int d, const int64_t *info, int b,
+                                 long long *removed_global) {
+  uint64_t amask = 0;
+  long long rem = 0;
+  for (int j = 0; j < d && j < 64; j++) {
+    const int64_t v = picks[(int64_t)b * d + j];
+    if (v < 0) continue;
+    int64_t deg = info[2 * ((int64_t)b * d + j)];
+    const uint64_t adj = (uint64_t)info[2 * ((int64_t)b * d + j) + 1];
+    if (j > 0) deg -= __popcll(adj & amask);
+    if (j == 0 || deg > 0) {
+      amask |= 1ull << j;
+      rem += 2 * deg;
+    }
+  }
+  *removed_global = rem;
+  return amask;
+}
+
+// Phase 2 (every rank): replay, then remove the accepted picks' rows (owner)
+// and columns (every rank) in parallel.  Entries are killed with atomicOr so
+// an edge between two accepted picks is counted exactly once; rdeg is
+// decremented atomically.  grid = (chunks, B).
 __global__ void apply_phase2_kernel(s2v_shard sh, const int64_t *picks, int d,
                                     const int64_t *info, uint8_t *applied, int64_t *removed) {
-  const int b = blockIdx.x;
-  __shared__ unsigned long long s_removed_local;
-  __shared__ uint64_t s_applied_mask;
+  const int b = blockIdx.y;
+  __shared__ uint64_t s_amask;
+  __shared__ unsigned long long s_local;
   if (threadIdx.x == 0) {
-    uint64_t amask = 0;
-    long long rem_global = 0;
-    for (int j = 0; j < d; j++) {
-      int64_t v = picks[(int64_t)b * d + j];
-      bool ok = false;
-      if (v >= 0) {
-        int64_t deg = info[2 * ((int64_t)b * d + j)];
-        uint64_t adj = (uint64_t)info[2 * ((int64_t)b * d + j) + 1];
-        if (j > 0) deg -= __popcll(adj & amask);
-        ok = (j == 0) || deg > 0;
-        if (ok) rem_global += 2 * deg;
-      }
-      if (ok && j < 64) amask |= 1ull << j;
-      applied[(int64_t)b * d + j] = ok ? 1 : 0;
+    long long rem = 0;
+    s_amask = replay_group(picks, d, info, b, &rem);
+    s_local = 0;
+    if (blockIdx.x == 0) {
+      removed[b] = rem;
+      for (int j = 0; j < d; j++)
+        applied[(int64_t)b * d + j] = (j < 64 && ((s_amask >> j) & 1ull)) ? 1 : 0;
     }
-    s_applied_mask = amask;
-    s_removed_local = 0;
-    removed[b] = rem_global;
   }
   __syncthreads();
-  const uint64_t amask = s_applied_mask;
+  const uint64_t amask = s_amask;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   unsigned long long local = 0;
   for (int j = 0; j < d && j < 64; j++) {
     if (!((amask >> j) & 1ull)) continue;
     const int64_t v = picks[(int64_t)b * d + j];
-    // row v (owner only)
     if (v >= sh.row_start && v < sh.row_start + sh.num_rows) {
       const int64_t r = (int64_t)b * sh.num_rows + (v - sh.row_start);
-      for (int64_t e = sh.row_ptr[r] + threadIdx.x; e < sh.row_ptr[r + 1]; e += blockDim.x) {
-        uint32_t c = sh.cols[e];
-        if (!(c & S2V_DEAD)) {
-          sh.cols[e] = c | S2V_DEAD;
+      for (int64_t e = sh.row_ptr[r] + tid; e < sh.row_ptr[r + 1]; e += stride) {
+        const uint32_t old = atomicOr(sh.cols + e, S2V_DEAD);
+        if (!(old & S2V_DEAD)) {
           local++;
+          atomicSub(sh.rdeg + r, 1);
         }
       }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        sh.rdeg[r] = 0;
+      if (tid == 0) {
         sh.sol[r] = 1;
         sh.cand[r] = 0;
       }
     }
-    // column v: each local row holds at most one entry whose neighbour is v
     const int64_t cb = (int64_t)b * sh.num_nodes + v;
-    for (int64_t k = sh.col_ptr[cb] + threadIdx.x; k < sh.col_ptr[cb + 1]; k += blockDim.x) {
-      int64_t e = sh.col_ent[k];
-      uint32_t c = sh.cols[e];
-      if (!(c & S2V_DEAD)) {
-        sh.cols[e] = c | S2V_DEAD;
+    for (int64_t q = sh.col_ptr[cb] + tid; q < sh.col_ptr[cb + 1]; q += stride) {
+      const int64_t e = sh.col_ent[q];
+      const uint32_t old = atomicOr(sh.cols + e, S2V_DEAD);
+      if (!(old & S2V_DEAD)) {
         local++;
-        int32_t row = sh.col_row[k];
-        int32_t nd = sh.rdeg[row] - 1;
-        sh.rdeg[row] = nd;
-        sh.cand[row] = (nd > 0 && !sh.sol[row]) ? 1 : 0;
+        atomicSub(sh.rdeg + sh.col_row[q], 1);
       }
     }
-    __syncthreads();
   }
-  if (local) atomicAdd(&s_removed_local, local);
+  if (local) atomicAdd(&s_local, local);
   __syncthreads();
-  if (threadIdx.x == 0) sh.residual[b] -= (int64_t)s_removed_local;
+  if (threadIdx.x == 0 && s_local)
+    atomicAdd((unsigned long long *)&sh.residual[b], (unsigned long long)(-(long long)s_local));
+}
+
+// Phase 3: candidacy of the rows touched by the accepted picks
+// (state.py:206-208 recomputes all row sums; only these rows can change).
+__global__ void apply_phase3_kernel(s2v_shard sh, const int64_t *picks, int d,
+                                    const uint8_t *applied) {
+  const int b = blockIdx.y;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int j = 0; j < d && j < 64; j++) {
+    if (!applied[(int64_t)b * d + j]) continue;
+    const int64_t v = picks[(int64_t)b * d + j];
+    const int64_t cb = (int64_t)b * sh.num_nodes + v;
+    for (int64_t q = sh.col_ptr[cb] + tid; q < sh.col_ptr[cb + 1]; q += stride) {
+      const int32_t row = sh.col_row[q];
+      sh.cand[row] = (sh.rdeg[row] > 0 && !sh.sol[row]) ? 1 : 0;
+    }
+  }
 }
 
 }  // namespace s2v
@@ -235,8 +261,10 @@ int s2v_apply_phase1(const s2v_shard *sh, const int64_t *picks, int d, int64_t *
 int s2v_apply_phase2(const s2v_shard *sh, const int64_t *picks, int d, const int64_t *info,
                      uint8_t *applied, int64_t *removed, void *stream) {
   if (d < 1 || d > 64) return fail(S2V_EINVAL, "group size d=%d outside [1, 64]", d);
-  apply_phase2_kernel<<<sh->batch, 256, 0, as_stream(stream)>>>(*sh, picks, d, info, applied,
-                                                                removed);
+  dim3 grid(16, sh->batch);
+  apply_phase2_kernel<<<grid, 256, 0, as_stream(stream)>>>(*sh, picks, d, info, applied, removed);
+  S2V_LAUNCH_CHECK();
+  apply_phase3_kernel<<<grid, 256, 0, as_stream(stream)>>>(*sh, picks, d, applied);
   S2V_LAUNCH_CHECK();
   return S2V_OK;
 }

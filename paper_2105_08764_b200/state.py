@@ -96,6 +96,9 @@ class _ShardStructure:
         self.nnz = hi - lo
         self.rows = rows
         self.max_deg = int(np.diff(row_ptr).max()) if rows else 0
+        # descending-degree processing order (load balance of the round kernel)
+        self.order = to_device(np.argsort(-np.diff(row_ptr), kind="stable").astype(np.int32),
+                               device)
         self.row_ptr = to_device(row_ptr, device)
         self.cols0 = to_device(cols0, device)
         self.col_ptr = to_device(col_ptr, device)
@@ -164,6 +167,8 @@ class PartitionedState:
             if self.nnz else torch.zeros(1, dtype=torch.int64, device=dev)
         self.col_row = torch.cat([s.col_row + int(b * rows) for b, s in enumerate(structs)]) \
             if self.nnz else torch.zeros(1, dtype=torch.int32, device=dev)
+        self.order = torch.cat([s.order + int(b * rows) for b, s in enumerate(structs)]) \
+            if rows else torch.zeros(1, dtype=torch.int32, device=dev)
         nr = max(batch * rows, 1)
         self.rdeg = torch.zeros(nr, dtype=torch.int32, device=dev)
         self.sol_d = torch.zeros(nr, dtype=torch.uint8, device=dev)
@@ -174,7 +179,8 @@ class PartitionedState:
             row_start=part.row_start, num_rows=rows, rows_max=self.rows_max, nnz=self.nnz,
             row_ptr=ptr(self.row_ptr), cols=ptr(self.cols), col_ptr=ptr(self.col_ptr),
             col_ent=ptr(self.col_ent), col_row=ptr(self.col_row), rdeg=ptr(self.rdeg),
-            sol=ptr(self.sol_d), cand=ptr(self.cand_d), residual=ptr(self.residual_d))
+            sol=ptr(self.sol_d), cand=ptr(self.cand_d), residual=ptr(self.residual_d),
+            order=ptr(self.order))
         sol_phys = np.zeros((batch, P, self.rows_max), dtype=np.uint8)
         if P == 1:
             sol_phys[:, 0, :] = solutions
