@@ -196,6 +196,10 @@ int s2v_comm_allgather_slots(void *comm, void *recv, size_t bytes, size_t slot_s
                              int nslots, int rank, void *stream);
 int s2v_comm_allreduce(void *comm, void *buf, size_t count, int kind /*0 i64 1 f64 2 f32*/,
                        void *stream);
+/* cudaMemcpyAsync(..., cudaMemcpyDefault): the in-process thread-group
+ * transport (ranks as threads, possibly sharing one device) moves halo chunks
+ * with peer copies instead of NCCL. */
+int s2v_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -79,6 +79,7 @@ _SIGNATURES = {
     "s2v_comm_allgather": ([_P, _P, _P, _SZ, _P], _I),
     "s2v_comm_allgather_slots": ([_P, _P, _SZ, _SZ, _I, _I, _P], _I),
     "s2v_comm_allreduce": ([_P, _P, _SZ, _I, _P], _I),
+    "s2v_memcpy_async": ([_P, _P, _SZ, _P], _I),
     "s2v_generate_ba": ([_I64, _I64, _P, _P], _I64),
 }
 

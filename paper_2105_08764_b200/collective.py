@@ -38,7 +38,8 @@ class CollectiveStats:
 class WorkerGroup:
     """A fixed set of P cooperating thread-ranks and their rendezvous."""
 
-    def __init__(self, num_workers: int, timeout: float = DEFAULT_TIMEOUT):
+    def __init__(self, num_workers: int, timeout: float = DEFAULT_TIMEOUT,
+                 use_nccl: bool = False):
         if num_workers < 1:
             raise ValueError(f"num_workers must be >= 1, got {num_workers}")
         self.num_workers = int(num_workers)
@@ -47,7 +48,7 @@ class WorkerGroup:
         self._barrier = threading.Barrier(self.num_workers)
         self._stats: dict[str, CollectiveStats] = {}
         self._lock = threading.Lock()
-        self._nccl_id: bytes | None = None
+        self.use_nccl = bool(use_nccl)
 
     def comm(self, rank: int) -> "Comm":
         if not 0 <= rank < self.num_workers:
@@ -78,6 +79,14 @@ class WorkerGroup:
             raise CollectiveAborted(
                 f"collective aborted: a rank failed or did not arrive within "
                 f"{self.timeout:.1f}s (P={self.num_workers})") from None
+
+    def _exchange_objects(self, rank: int, value) -> list:
+        """Rank-ordered exchange of arbitrary Python objects (no copy)."""
+        self._slots[rank] = value
+        self._wait()
+        out = list(self._slots)
+        self._wait()
+        return out
 
     def _exchange(self, rank: int, value) -> list:
         # deposit a private copy, wait for everyone, snapshot, wait again so
@@ -113,6 +122,62 @@ class _DeviceComm:
         if self.handle:
             self._lib.load().s2v_comm_destroy(self.handle)
             self.handle = None
+
+
+class _LocalDeviceComm:
+    """Device transport for thread-ranks of one process (run_workers).
+
+    Ranks may share one GPU (tests on a single B200) or own one each.  The
+    in-place halo all-gather is done with peer copies ordered by CUDA events
+    exchanged through the host rendezvous; all-reduces of the small integer /
+    fp64 packs go through the host in ascending rank order (the reference's
+    own reduction order, collective.py:114-116).
+    """
+
+    def __init__(self, comm: "Comm"):
+        from . import _lib
+        self._lib = _lib
+        self.comm = comm
+        self.world, self.rank = comm.size, comm.rank
+
+    def _publish(self, value):
+        return self.comm.group._exchange_objects(self.rank, value)
+
+    def allgather_slots(self, buf_ptr: int, chunk_bytes: int, slot_stride: int, nslots: int,
+                        stream: int) -> None:
+        import torch
+        ready = torch.cuda.Event()
+        ready.record()
+        peers = self._publish((buf_ptr, ready))
+        for q, (peer_ptr, peer_ready) in enumerate(peers):
+            if q == self.rank:
+                continue
+            torch.cuda.current_stream().wait_event(peer_ready)
+            for b in range(nslots):
+                off = b * slot_stride + q * chunk_bytes
+                self._lib.call("s2v_memcpy_async", buf_ptr + off, peer_ptr + off, chunk_bytes,
+                               stream)
+        done = torch.cuda.Event()
+        done.record()
+        for q, ev in enumerate(self._publish(done)):
+            if q != self.rank:
+                torch.cuda.current_stream().wait_event(ev)
+
+    def allreduce(self, buf_ptr: int, count: int, kind: int, stream: int) -> None:
+        import torch
+        dt = {0: torch.int64, 1: torch.float64, 2: torch.float32}[kind]
+        host = torch.empty(count, dtype=dt)
+        self._lib.call("s2v_memcpy_async", host.data_ptr(), buf_ptr, count * host.element_size(),
+                       stream)
+        torch.cuda.current_stream().synchronize()
+        total = self.comm.all_reduce_sum(host.numpy().copy(), tag="device")
+        host.copy_(torch.from_numpy(np.ascontiguousarray(total, dtype=host.numpy().dtype)))
+        self._lib.call("s2v_memcpy_async", buf_ptr, host.data_ptr(), count * host.element_size(),
+                       stream)
+        torch.cuda.current_stream().synchronize()
+
+    def close(self) -> None:
+        pass
 
 
 def _new_unique_id() -> bytes:
@@ -173,14 +238,19 @@ class Comm:
         if self.rank == 0:
             self.group._record(tag, elements)
 
-    def device_comm(self) -> _DeviceComm | None:
-        """Lazily create this rank's NCCL communicator (None when P == 1)."""
+    def device_comm(self):
+        """This rank's device transport (None when P == 1): peer copies between
+        the thread-ranks of this process (_LocalDeviceComm), or NCCL when the
+        group was created with use_nccl=True and every rank owns a GPU."""
         if self.size == 1:
             return None
         if self._dev is None:
-            uid = _new_unique_id() if self.rank == 0 else b""
-            ids = self.group._exchange(self.rank, np.frombuffer(uid or b"\0", dtype=np.uint8))
-            self._dev = _DeviceComm(bytes(ids[0]), self.size, self.rank)
+            if getattr(self.group, "use_nccl", False):
+                uid = _new_unique_id() if self.rank == 0 else b""
+                ids = self.group._exchange(self.rank, np.frombuffer(uid or b"\0", dtype=np.uint8))
+                self._dev = _DeviceComm(bytes(ids[0]), self.size, self.rank)
+            else:
+                self._dev = _LocalDeviceComm(self)
         return self._dev
 
 

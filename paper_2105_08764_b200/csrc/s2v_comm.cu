@@ -62,6 +62,13 @@ int s2v_comm_allgather_slots(void *comm, void *recv, size_t bytes, size_t slot_s
   return S2V_OK;
 }
 
+// Plain async copy (device<->device across peers, or host<->device), used by
+// the in-process thread-group transport (collective._LocalDeviceComm).
+int s2v_memcpy_async(void *dst, const void *src, size_t bytes, void *stream) {
+  S2V_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)));
+  return S2V_OK;
+}
+
 int s2v_comm_allreduce(void *comm, void *buf, size_t count, int kind, void *stream) {
   ncclDataType_t t = kind == 0 ? ncclInt64 : (kind == 1 ? ncclFloat64 : ncclFloat32);
   ncclResult_t r = ncclAllReduce(buf, buf, count, t, ncclSum, (ncclComm_t)comm,

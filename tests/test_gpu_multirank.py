@@ -1,0 +1,97 @@
+"""Node-sharded (P > 1) execution on the GPU: P thread-ranks (sharing the one
+B200 of the test box, or one GPU each) run the row-partitioned shards with the
+in-process device transport.  The halo design makes every result bitwise
+P-invariant and equal to the P = 1 oracle -- stronger than the reference,
+whose rank-ordered partial sums differ across P."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2105_08764_b200 as P
+from oracle import cref, port
+from reference_math import scale_error
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_forward_bitwise_at_any_p(p):
+    g = P.generate_ba(1000, 4, 0)
+    params = P.PolicyParams.initialize(64, 5, seed=0)
+    sol = (np.random.default_rng(3).random(1000) < 0.1).astype(np.uint8)
+
+    def worker(comm):
+        part = P.partition_rows(1000, comm.size)[comm.rank]
+        st = P.PartitionedState([g], part, solutions=sol[None])
+        emb = P.embed_forward(st, params, comm)
+        sc = P.q_forward(emb, st.cand, params, comm)
+        return comm.all_gather(emb, axis=-1), comm.all_gather(sc, axis=-1)
+    outs = P.run_workers(p, worker)
+    rp, cols = g.csr_arrays()
+    h, _, _, _, sc = cref.forward(rp, cols, sol, params.as_dict(), 5)
+    for emb, scores in outs:
+        assert np.array_equal(emb[0].T, h)
+        assert np.array_equal(scores[0], sc)
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_solve_trajectory_is_the_p1_reference_at_any_p(p):
+    gold = np.load(GOLD / "solve_ba1000_k64_l5.npz")
+    g = P.generate_ba(1000, 4, 0)
+    params = P.PolicyParams.initialize(64, 5, seed=0)
+    res = P.run_workers(p, lambda comm: P.solve([g], params, comm))
+    for (r,) in res:
+        assert r.cover == gold["covers"].tolist()
+        assert r.policy_evals == int(gold["evals"][0])
+        assert r.skipped == int(gold["skipped"][0])
+
+
+def test_batched_solve_p3():
+    gold = np.load(GOLD / "solve_batch3_k32_l2.npz")
+    graphs = [P.generate_ba(800, 4, s) for s in (1, 2, 3)]
+    params = P.PolicyParams.initialize(32, 2, seed=1)
+    res = P.run_workers(3, lambda comm: P.solve(graphs, params, comm))[0]
+    offs = np.concatenate([[0], np.cumsum(gold["cover_lens"])])
+    for b, r in enumerate(res):
+        assert r.cover == gold["covers"][offs[b]:offs[b + 1]].tolist()
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_gradients_p_invariant_and_replicas_identical(p):
+    rng = np.random.default_rng(7)
+    n, B, K, L = 300, 3, 16, 3
+    graphs = [P.generate_ba(n, 3, 70 + i) for i in range(B)]
+    sols = (rng.random((B, n)) < 0.15).astype(np.uint8)
+    ps = port.ResidualState([g.edge_array for g in graphs], n, solutions=sols)
+    actions = np.array([int(np.flatnonzero(ps.cand[b])[0]) for b in range(B)])
+    targets = rng.normal(size=B).astype(np.float32)
+    params = P.PolicyParams.initialize(K, L, seed=2, orientation="symmetric")
+
+    def worker(comm):
+        part = P.partition_rows(n, comm.size)[comm.rank]
+        st = P.PartitionedState(graphs, part, solutions=sols)
+        return P.loss_and_gradients(st, actions, targets, params, comm)
+    base_loss, base = P.run_workers(1, worker)[0]
+    outs = P.run_workers(p, worker)
+    for loss, grads in outs:
+        assert abs(loss - base_loss) <= 1e-6 * max(1.0, abs(base_loss))
+        for k in P.PARAM_NAMES:
+            assert scale_error(grads[k], base[k]).max() < 1e-5, k
+    for loss, grads in outs[1:]:
+        assert loss == outs[0][0]
+        for k in P.PARAM_NAMES:
+            assert np.array_equal(grads[k], outs[0][1][k])
+
+
+def test_owner_side_rejection_under_p2():
+    g = P.Graph(4, [(0, 1), (1, 2), (2, 3)])
+
+    def worker(comm):
+        part = P.partition_rows(4, comm.size)[comm.rank]
+        st = P.PartitionedState([g], part)
+        st.apply_action(1)
+        st.apply_action(1)
+    with pytest.raises(P.InvalidActionError, match="already in the solution"):
+        P.run_workers(2, worker)
