@@ -356,6 +356,19 @@ def decode_keys(top: np.ndarray):
     return node, vals, valid
 
 
+def merge_rank_keys(top: np.ndarray, counts: np.ndarray, comm, d: int):
+    """Merge every rank's top-d keys (B, d, 2) and candidate counts into the
+    global top-d, identically on every rank (replaces the reference's
+    all_gather of the full (B, N) score matrix, inference.py:113).  Keys
+    order by score image then ~node, so the merge keeps descending score
+    with lowest-index ties."""
+    b = top.shape[0]
+    keys = comm.all_gather(top.reshape(b, -1), axis=-1, tag="select").reshape(b, -1, 2)
+    counts = comm.all_reduce_sum(counts, tag="select")
+    order = np.lexsort((keys[..., 1], keys[..., 0]), axis=-1)[:, ::-1][:, :d]
+    return np.take_along_axis(keys, order[..., None], axis=1), counts
+
+
 def evaluate(state: PartitionedState, params: PolicyParams, comm, d: int, mode: int = 0):
     """Fused policy evaluation for the selection loops: embed + score + top-d
     keys, nothing but keys and counts leave the device.  Returns
@@ -365,12 +378,7 @@ def evaluate(state: PartitionedState, params: PolicyParams, comm, d: int, mode: 
     emb = DeviceEmbedding(state, hs[-1], params.embed_dim, params.dtype, gathered=True)
     _, top, counts = _score(emb, params, dparams, None, mode, d)
     if state.world > 1:
-        # merge per-rank top-d keys identically on every rank
-        keys = comm.all_gather(top.reshape(state.batch, -1), axis=-1, tag="select")
-        keys = keys.reshape(state.batch, -1, 2)
-        counts = comm.all_reduce_sum(counts, tag="select")
-        order = np.lexsort((keys[..., 1], keys[..., 0]), axis=-1)[:, ::-1][:, :d]
-        top = np.take_along_axis(keys, order[..., None], axis=1)
+        top, counts = merge_rank_keys(top, counts, comm, d)
     nodes, vals, valid = decode_keys(top)
     return nodes, vals, valid, counts
 
