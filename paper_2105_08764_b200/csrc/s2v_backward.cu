@@ -15,6 +15,7 @@
 // replicas on every rank.  Adam follows the reference's element-wise fp32
 // rounding sequence exactly.
 #include "s2v_common.cuh"
+#include "s2v_gather.cuh"
 
 namespace s2v {
 
@@ -315,10 +316,258 @@ __global__ void adam_kernel(T *__restrict__ p, const T *__restrict__ g, T *__res
   }
 }
 
+// ---------------------------------------------------------------------------
+// K = 64 fp32 fast paths (tiles of 64 rows, 4x4 register tiles).
+// ---------------------------------------------------------------------------
+constexpr int kT64 = 64;
+
+__device__ __forceinline__ float4 f4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+__device__ __forceinline__ void st4(float *p, const float4 &v) {
+  *reinterpret_cast<float4 *>(p) = v;
+}
+
+// dz = grad_h * (h_l > 0); dzsum (+)= dz; P4 (+)= dz^T m; dm = dz theta4
+// (dm[row][j] = sum_k theta4[k][j] dz[row][k]).  Dynamic smem: 3 x [64][68].
+__global__ void __launch_bounds__(256, 2) layer_backward64_kernel(
+    s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ grad_h,
+    const float *__restrict__ h_l, const float *__restrict__ m_l, float *__restrict__ dzsum,
+    float *__restrict__ partial, int first, float *__restrict__ dm_out) {
+  extern __shared__ __align__(16) float smem_f[];
+  float(*th4)[68] = reinterpret_cast<float(*)[68]>(smem_f);
+  float(*dzs)[68] = reinterpret_cast<float(*)[68]>(smem_f + 64 * 68);
+  float(*ms)[68] = reinterpret_cast<float(*)[68]>(smem_f + 2 * 64 * 68);
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < 64 * 64; idx += 256) th4[idx / 64][idx % 64] = theta4[idx];
+  const int lo = tid & 15, hi = tid >> 4;
+  float p4[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+      p4[a][c] = first ? 0.f : partial[(int64_t)blockIdx.x * 4096 + (4 * lo + a) * 64 + 4 * hi + c];
+  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  const int64_t ntiles = (nrows + kT64 - 1) / kT64;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kT64;
+    __syncthreads();
+    for (int e = tid; e < kT64 * 16; e += 256) {
+      const int row = e >> 4, c4 = e & 15;
+      const int64_t r = r0 + row;
+      float4 dz = make_float4(0.f, 0.f, 0.f, 0.f), mv = dz;
+      if (r < nrows) {
+        const float4 g = f4(grad_h + r * 64 + 4 * c4);
+        const float4 hv = f4(h_l + phys_of_row(sh, r) * 64 + 4 * c4);
+        dz.x = hv.x > 0.f ? g.x : 0.f;
+        dz.y = hv.y > 0.f ? g.y : 0.f;
+        dz.z = hv.z > 0.f ? g.z : 0.f;
+        dz.w = hv.w > 0.f ? g.w : 0.f;
+        float *ds = dzsum + r * 64 + 4 * c4;
+        if (first) {
+          st4(ds, dz);
+        } else {
+          float4 o = f4(ds);
+          o.x += dz.x;
+          o.y += dz.y;
+          o.z += dz.z;
+          o.w += dz.w;
+          st4(ds, o);
+        }
+        if (m_l) mv = f4(m_l + r * 64 + 4 * c4);
+      }
+      st4(&dzs[row][4 * c4], dz);
+      st4(&ms[row][4 * c4], mv);
+    }
+    __syncthreads();
+    if (m_l) {
+#pragma unroll 4
+      for (int row = 0; row < kT64; row++) {
+        const float4 d = f4(&dzs[row][4 * lo]);
+        const float4 m = f4(&ms[row][4 * hi]);
+        const float dv[4] = {d.x, d.y, d.z, d.w}, mvv[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int c = 0; c < 4; c++) p4[a][c] = __fmaf_rn(dv[a], mvv[c], p4[a][c]);
+      }
+    }
+    if (dm_out) {
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) acc[a][c] = 0.f;
+#pragma unroll 4
+      for (int k = 0; k < 64; k++) {
+        const float4 t = f4(&th4[k][4 * lo]);
+#pragma unroll
+        for (int a = 0; a < 4; a++) {
+          const float d = dzs[4 * hi + a][k];
+          acc[a][0] = __fmaf_rn(t.x, d, acc[a][0]);
+          acc[a][1] = __fmaf_rn(t.y, d, acc[a][1]);
+          acc[a][2] = __fmaf_rn(t.z, d, acc[a][2]);
+          acc[a][3] = __fmaf_rn(t.w, d, acc[a][3]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; a++) {
+        const int64_t r = r0 + 4 * hi + a;
+        if (r < nrows)
+          st4(dm_out + phys_of_row(sh, r) * 64 + 4 * lo,
+              make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]));
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+      partial[(int64_t)blockIdx.x * 4096 + (4 * lo + a) * 64 + 4 * hi + c] = p4[a][c];
+}
+
+// dtheta1 [64], dtheta2 [64], dtheta3 [64][64] partials from dzsum.
+// Dynamic smem: th3 [64][68], dzs [64][68], ws [64][68], red [16][64], aux.
+__global__ void __launch_bounds__(256, 2) param_grads64_kernel(
+    s2v_shard sh, const float *__restrict__ theta2, const float *__restrict__ theta3,
+    const float *__restrict__ dzsum, float *__restrict__ partial) {
+  extern __shared__ __align__(16) float smem_f[];
+  float(*th3)[68] = reinterpret_cast<float(*)[68]>(smem_f);
+  float(*dzs)[68] = reinterpret_cast<float(*)[68]>(smem_f + 64 * 68);
+  float(*ws)[68] = reinterpret_cast<float(*)[68]>(smem_f + 2 * 64 * 68);
+  float(*red)[64] = reinterpret_cast<float(*)[64]>(smem_f + 3 * 64 * 68);
+  float *s_sol = smem_f + 3 * 64 * 68 + 16 * 64;
+  float *s_deg = s_sol + 64;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < 64 * 64; idx += 256) th3[idx / 64][idx % 64] = theta3[idx];
+  const int lo = tid & 15, hi = tid >> 4;
+  float p3[4][4], p2[4], p1 = 0.f;
+#pragma unroll
+  for (int a = 0; a < 4; a++) {
+    p2[a] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; c++) p3[a][c] = 0.f;
+  }
+  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  const int64_t ntiles = (nrows + kT64 - 1) / kT64;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kT64;
+    __syncthreads();
+    if (tid < kT64) {
+      const int64_t r = r0 + tid;
+      const bool ok = r < nrows;
+      s_sol[tid] = (ok && sh.sol[r]) ? 1.f : 0.f;
+      s_deg[tid] = (ok && !sh.sol[r]) ? (float)sh.rdeg[r] : 0.f;
+    }
+    __syncthreads();
+    for (int e = tid; e < kT64 * 16; e += 256) {
+      const int row = e >> 4, c4 = e & 15;
+      const int64_t r = r0 + row;
+      const float4 d = r < nrows ? f4(dzsum + r * 64 + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      st4(&dzs[row][4 * c4], d);
+      const float deg = s_deg[row];
+      float4 w;
+      w.x = relu(theta2[4 * c4 + 0] * deg);
+      w.y = relu(theta2[4 * c4 + 1] * deg);
+      w.z = relu(theta2[4 * c4 + 2] * deg);
+      w.w = relu(theta2[4 * c4 + 3] * deg);
+      st4(&ws[row][4 * c4], w);
+    }
+    __syncthreads();
+    // dtheta3[k][j] += dz[row][k] w[row][j]   (k = 4lo+a, j = 4hi+c)
+#pragma unroll 4
+    for (int row = 0; row < kT64; row++) {
+      const float4 d = f4(&dzs[row][4 * lo]);
+      const float4 w = f4(&ws[row][4 * hi]);
+      const float dv[4] = {d.x, d.y, d.z, d.w}, wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) p3[a][c] = __fmaf_rn(dv[a], wv[c], p3[a][c]);
+    }
+    // dtheta2[j] += deg (w_j > 0) (theta3^T dz)_j   rows 4hi+a, j = 4lo+c
+    {
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) acc[a][c] = 0.f;
+#pragma unroll 4
+      for (int k = 0; k < 64; k++) {
+        const float4 t = f4(&th3[k][4 * lo]);
+#pragma unroll
+        for (int a = 0; a < 4; a++) {
+          const float d = dzs[4 * hi + a][k];
+          acc[a][0] = __fmaf_rn(t.x, d, acc[a][0]);
+          acc[a][1] = __fmaf_rn(t.y, d, acc[a][1]);
+          acc[a][2] = __fmaf_rn(t.z, d, acc[a][2]);
+          acc[a][3] = __fmaf_rn(t.w, d, acc[a][3]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; a++) {
+        const int row = 4 * hi + a;
+        const float deg = s_deg[row];
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+          if (ws[row][4 * lo + c] > 0.f) p2[c] = __fmaf_rn(acc[a][c], deg, p2[c]);
+      }
+    }
+    // dtheta1[k] += dz[row][k] sol[row]
+    if (tid < 64)
+      for (int row = 0; row < kT64; row++) p1 = __fmaf_rn(dzs[row][tid], s_sol[row], p1);
+  }
+  __syncthreads();
+  // reduce p2 over the 16 row groups (hi), then write the partial row
+#pragma unroll
+  for (int c = 0; c < 4; c++) red[hi][4 * lo + c] = p2[c];
+  __syncthreads();
+  float *out = partial + (int64_t)blockIdx.x * (2 * 64 + 4096);
+  if (tid < 64) {
+    float s2 = 0.f;
+    for (int q = 0; q < 16; q++) s2 += red[q][tid];
+    out[tid] = p1;
+    out[64 + tid] = s2;
+  }
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int c = 0; c < 4; c++) out[128 + (4 * lo + a) * 64 + 4 * hi + c] = p3[a][c];
+}
+
+// spmm_t for K = 64 fp32: half-warp per row in descending-degree order.
+__global__ void __launch_bounds__(256) gather64_kernel(s2v_shard sh,
+                                                       const float *__restrict__ src,
+                                                       float *__restrict__ out,
+                                                       uint32_t hot_rows) {
+  const int tid = threadIdx.x, sub = tid & 15;
+  const unsigned hmask = (tid & 16) ? 0xFFFF0000u : 0x0000FFFFu;
+  const int hbase = tid & 16;
+  const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
+  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  const int64_t nhw = ((int64_t)gridDim.x * blockDim.x) >> 4;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + tid) >> 4; q < nrows; q += nhw) {
+    const int64_t r = sh.order ? sh.order[q] : q;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!sh.sol[r])
+      acc = gather_row64(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, src, sub, hmask, hbase,
+                         hot_rows, pol_hot, pol_cold);
+    st4(out + r * 64 + 4 * sub, acc);
+  }
+}
+
 template <class T>
 static int layer_backward_t(const s2v_shard *sh, int K, const void *theta4, const void *grad_h,
                             const void *h_l, const void *m_l, void *dzsum, void *partial,
                             int first, void *dm_out, cudaStream_t st) {
+  if (sizeof(T) == 4 && K == 64) {
+    const size_t smem = sizeof(float) * 3 * 64 * 68;
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(layer_backward64_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    layer_backward64_kernel<<<bwd_blocks(*sh), 256, smem, st>>>(
+        *sh, (const float *)theta4, (const float *)grad_h, (const float *)h_l,
+        (const float *)m_l, (float *)dzsum, (float *)partial, first, (float *)dm_out);
+    S2V_LAUNCH_CHECK();
+    return S2V_OK;
+  }
   if (K * K > 64 * kBwdThreads) return fail(S2V_EINVAL, "embed_dim %d too large for backward", K);
   size_t smem = sizeof(T) * ((size_t)K * (K + 1) + 2 * kBwdTile * (size_t)K);
   auto kern = layer_backward_kernel<T>;
@@ -368,6 +617,12 @@ int s2v_gather(s2v_dtype dt, const s2v_shard *sh, int K, const void *src, void *
                void *stream) {
   int64_t rows = (int64_t)sh->batch * sh->num_rows;
   if (rows == 0) return S2V_OK;
+  if (dt == S2V_F32 && K == 64) {
+    gather64_kernel<<<kNumSMs * 8, 256, 0, as_stream(stream)>>>(
+        *sh, (const float *)src, (float *)out, (uint32_t)((48ull << 20) / 256));
+    S2V_LAUNCH_CHECK();
+    return S2V_OK;
+  }
   int grid = (int)std::min<int64_t>((rows * 32 + 255) / 256, kNumSMs * 16);
   if (dt == S2V_F32)
     gather_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(*sh, K, (const float *)src,
@@ -385,7 +640,14 @@ int s2v_param_grads(s2v_dtype dt, const s2v_shard *sh, int K, const void *theta2
   size_t elem = dt == S2V_F32 ? 4 : 8;
   size_t smem = elem * ((size_t)K * (K + 1) + 2 * kBwdTile * (size_t)K + 2 * kBwdTile);
   cudaStream_t st = as_stream(stream);
-  if (dt == S2V_F32) {
+  if (dt == S2V_F32 && K == 64) {
+    const size_t smem64 = sizeof(float) * (3 * 64 * 68 + 16 * 64 + 128);
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(param_grads64_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64));
+    param_grads64_kernel<<<bwd_blocks(*sh), 256, smem64, st>>>(
+        *sh, (const float *)theta2, (const float *)theta3, (const float *)dzsum,
+        (float *)partials);
+  } else if (dt == S2V_F32) {
     auto kern = param_grads_kernel<float>;
     S2V_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<bwd_blocks(*sh), kBwdThreads, smem, st>>>(*sh, K, (const float *)theta2,
