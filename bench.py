@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--m", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--train-steps", type=int, default=5)
     return ap.parse_args()
 
 
@@ -171,6 +173,83 @@ def run_reference(args):
             "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# training-step legs (BASELINE configs[1] and configs[3])
+# ---------------------------------------------------------------------------
+
+
+def _train_buffer(P, dataset, B, seed=0, frac=0.01):
+    """B replay tuples (one per batch slot): snapshot ~ Bernoulli(frac), action
+    a uniformly drawn candidate."""
+    rng = np.random.default_rng(seed)
+    buf = P.ReplayBuffer(max(B, 1))
+    for i in range(B):
+        gi = i % len(dataset)
+        g = dataset[gi]
+        bits = (rng.random(g.num_nodes) < frac).astype(np.uint8)
+        rp, cols = g.csr_arrays()
+        deg = np.diff(rp)
+        cands = np.flatnonzero((deg > 0) & (bits == 0))
+        buf.add(P.ExperienceTuple(gi, P.pack_solution(bits), int(cands[rng.integers(len(cands))]),
+                                  0.0))
+    return buf
+
+
+def train_leg(P, comm, dataset, B, tau, steps, warmup, name):
+    """Time train_step (public API: sample, tuples_to_graphs, batch_targets,
+    tau x (loss_and_gradients + adam_step)) with CUDA events."""
+    import torch
+    n = dataset[0].num_nodes
+    part = P.partition_rows(n, comm.size)[comm.rank]
+    buf = _train_buffer(P, dataset, B)
+    params = P.PolicyParams.initialize(64, 5, seed=0)
+    adam = P.AdamState.create(params, lr=1e-5)
+    cfg = P.TrainConfig(embed_dim=64, num_layers=5, batch_size=B, tau=tau)
+    rng = np.random.default_rng(7)
+    for _ in range(warmup):
+        P.train_step(buf, dataset, params, adam, cfg, rng, comm, part)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    losses = []
+    for _ in range(steps):
+        losses = P.train_step(buf, dataset, params, adam, cfg, rng, comm, part)
+    e1.record()
+    torch.cuda.synchronize()
+    return {"workload": name, "value": e0.elapsed_time(e1) / steps / 1e3, "unit": "s",
+            "B": B, "tau": tau, "steps": steps, "warmup": warmup,
+            "last_losses": [float(x) for x in losses],
+            "path": "train_step(buffer, dataset, params, adam, cfg, rng, comm, part)"}
+
+
+def cpu_train_sample(dataset, B_sample, B, tau):
+    """Reference algorithm (oracle/port.py) training step on B_sample of the B
+    tuples, scaled by B / B_sample (the step is linear in B)."""
+    from oracle import port
+    import paper_2105_08764_b200 as P
+    n = dataset[0].num_nodes
+    buf = _train_buffer(P, dataset, B)
+    tuples = [buf[i] for i in range(B_sample)]
+    theta = P.PolicyParams.initialize(64, 5, seed=0).as_dict()
+    edges = [dataset[t.graph_index].edge_array for t in tuples]
+    snaps = np.stack([P.unpack_solution(t.solution_snapshot, n) for t in tuples])
+    acts = np.array([t.action for t in tuples])
+    t0 = time.perf_counter()
+    st = port.ResidualState(edges, n, solutions=snaps)
+    tg = port.batch_targets(edges, n, snaps, acts, theta, 5, 0.9).astype(np.float32)
+    m = {k: np.zeros_like(v) for k, v in theta.items()}
+    v = {k: np.zeros_like(x) for k, x in theta.items()}
+    step = 0
+    for _ in range(tau):
+        _, grads = port.loss_and_grads(st, acts, tg, theta, 5)
+        step = port.adam(theta, grads, m, v, step, 1e-5)
+    dt = time.perf_counter() - t0
+    return {"value": dt * B / B_sample, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"oracle/port.py train step on {B_sample} of {B} tuples (tuples_to_graphs + "
+                      f"batch_targets + {tau} x (loss_and_grads + adam)) = {dt:.2f}s, "
+                      f"scaled x{B / B_sample:g}"}
 
 
 # ---------------------------------------------------------------------------
@@ -302,6 +381,21 @@ def main():
                "sample": "oracle/port.py (reference numpy/scipy algorithm) on the same graph: "
                          f"1 timed embedding round x 5 + q + select + apply; {detail}"}
 
+    train = None
+    if not args.no_train:
+        train = []
+        ds2 = [P.generate_ba(10000, 4, 100 + i) for i in range(32)]
+        leg2 = train_leg(P, comm, ds2, 32, 4, args.train_steps, args.warmup,
+                         "MVC DQN training step, 32 x BA(10000,4,seed=100+i), K=64, T=5, tau=4 "
+                         "(BASELINE configs[1])")
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            leg2["cpu_baseline"] = cpu_train_sample(ds2, 4, 32, 4)
+        train.append(leg2)
+        leg4 = train_leg(P, comm, [graph], 8, 4, max(2, args.train_steps // 2), 2,
+                         f"MVC DQN training step, 8 tuples of BA({args.nodes},{args.m},0) "
+                         "(node-level batch), K=64, T=5, tau=4 (BASELINE configs[3])")
+        train.append(leg4)
+
     if rank == 0:
         line = {"metric": METRIC, "value": step_ms / 1e3, "unit": "s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
@@ -309,6 +403,7 @@ def main():
                 "dtype": "f32", "data": "synthetic", "config": workload(args),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks.summary(),
+                "train_steps": train,
                 "setup": {"graph_gen_s": round(t_gen, 2), "state_build_s": round(t_state, 3),
                           "alive_entries_at_start": alive_entries}}
         print(json.dumps(line), flush=True)
