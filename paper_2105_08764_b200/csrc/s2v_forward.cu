@@ -546,30 +546,43 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
   const int64_t base_r = (int64_t)b * sh.num_rows;
   const int64_t base_phys = ((int64_t)b * sh.world + sh.rank) * sh.rows_max;
   const int kq = tid & 15, rq = tid >> 4;
-  for (int64_t t0 = i0; t0 < i1; t0 += kScoreTile) {
-    __syncthreads();
-    // load x = h * cand (fl(h*1) = h, fl(h*0) = +-0)
-    for (int e = tid; e < kScoreTile * 16; e += 256) {
+  // software pipeline: the next tile's rows are loaded into registers while
+  // the current tile is projected
+  float4 pre[4];
+  uint8_t pre_c[4];
+  auto load_tile = [&](int64_t t0) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int e = tid + q * 256;
       const int row = e >> 4, k4 = e & 15;
       const int64_t i = t0 + row;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      float c = 0.f;
-      if (i < i1) {
-        const uint8_t cb = cand_override ? cand_override[base_r + i] : sh.cand[base_r + i];
-        c = cb ? 1.f : 0.f;
-        if (k4 == 0) s_c[row] = cb;
-        v = *reinterpret_cast<const float4 *>(h + (base_phys + i) * 64 + k4 * 4);
-      } else if (k4 == 0) {
-        s_c[row] = 0;
+      pre[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      pre_c[q] = 0;
+      if (t0 < i1 && i < i1) {
+        pre_c[q] = cand_override ? cand_override[base_r + i] : sh.cand[base_r + i];
+        pre[q] = ldg_f4_pol(h + (base_phys + i) * 64 + k4 * 4, l2_policy_first());
       }
+    }
+  };
+  load_tile(i0);
+  for (int64_t t0 = i0; t0 < i1; t0 += kScoreTile) {
+    __syncthreads();
+    // x = h * cand (fl(h*1) = h, fl(h*0) = +-0)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int e = tid + q * 256;
+      const int row = e >> 4, k4 = e & 15;
+      const float c = pre_c[q] ? 1.f : 0.f;
+      if (k4 == 0) s_c[row] = pre_c[q];
       float4 x;
-      x.x = __fmul_rn(v.x, c);
-      x.y = __fmul_rn(v.y, c);
-      x.z = __fmul_rn(v.z, c);
-      x.w = __fmul_rn(v.w, c);
+      x.x = __fmul_rn(pre[q].x, c);
+      x.y = __fmul_rn(pre[q].y, c);
+      x.z = __fmul_rn(pre[q].z, c);
+      x.w = __fmul_rn(pre[q].w, c);
       *reinterpret_cast<float4 *>(&xs[row][k4 * 4]) = x;
     }
     __syncthreads();
+    load_tile(t0 + kScoreTile);
     float acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; a++)

@@ -282,8 +282,8 @@ class PartitionedState:
         ws = self.workspace("apply", d, lambda: {
             "picks": torch.empty(B * d, dtype=torch.int64, device=self.device),
             "info": torch.empty(2 * B * d, dtype=torch.int64, device=self.device),
-            "applied": torch.empty(B * d, dtype=torch.uint8, device=self.device),
-            "removed": torch.empty(B, dtype=torch.int64, device=self.device)})
+            # one read-back: [removed B | residual B | applied B*d bytes]
+            "out": torch.empty(2 * B + (B * d + 7) // 8, dtype=torch.int64, device=self.device)})
         ws["picks"].copy_(torch.from_numpy(picks.reshape(-1)), non_blocking=False)
         st = stream_ptr()
         _lib.call("s2v_apply_phase1", self.shard_ref(), ptr(ws["picks"]), d, ptr(ws["info"]), 0,
@@ -293,11 +293,16 @@ class PartitionedState:
             if dc is None:
                 raise InvalidActionError("a sharded state needs its comm to apply picks")
             dc.allreduce(ptr(ws["info"]), ws["info"].numel(), 0, st)
+        out = ws["out"]
+        base = out.data_ptr()
         _lib.call("s2v_apply_phase2", self.shard_ref(), ptr(ws["picks"]), d, ptr(ws["info"]),
-                  ptr(ws["applied"]), ptr(ws["removed"]), st)
+                  base + 16 * B, base, st)
+        _lib.call("s2v_memcpy_async", base + 8 * B, ptr(self.residual_d), 8 * B, st)
         self.invalidate()
-        applied = ws["applied"].to("cpu").numpy().reshape(B, d).astype(bool)
-        removed = ws["removed"].to("cpu").numpy().copy()
+        host = out.to("cpu").numpy()
+        removed = host[:B].copy()
+        self._host["residual"] = host[B:2 * B].copy()
+        applied = host[2 * B:].view(np.uint8)[:B * d].reshape(B, d).astype(bool)
         return applied, removed
 
     # -- termination (state.py:212-220) ------------------------------------------
