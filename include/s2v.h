@@ -68,9 +68,13 @@ typedef struct {
   uint8_t *sol;            /* [B*num_rows] partial solution S               */
   uint8_t *cand;           /* [B*num_rows] candidate set C                  */
   int64_t *residual;       /* [B] alive local entries                       */
-  const int32_t *order;    /* [B*num_rows] processing order (descending
-                              degree) for load balance; NULL = identity    */
+  const int32_t *order;    /* [B*num_rows] processing order: the n_hub hub
+                              rows (degree > S2V_HUB_DEGREE) first, then the
+                              rest, each by descending degree; NULL = identity */
+  int64_t n_hub;           /* rows handled by the CTA-cooperative hub kernel */
 } s2v_shard;
+
+#define S2V_HUB_DEGREE 4096
 
 /* ---- library ------------------------------------------------------------ */
 const char *s2v_last_error(void);
@@ -185,6 +189,13 @@ int s2v_adam(s2v_dtype dt, void *params, const void *grads, void *m, void *v, in
 /* Bit-exact generate_ba from numpy's PCG64 state {state_hi, state_lo, inc_hi,
  * inc_lo, has_uint32, uinteger} (host memory).  edges_out == NULL returns E. */
 int64_t s2v_generate_ba(int64_t n, int64_t d, const void *pcg, void *edges_out);
+/* R-MAT scale/edge_factor (BASELINE cfg5; graphs.generate_rmat's definition,
+ * the reference has none); edges_out holds edge_factor*2^scale pairs. */
+int64_t s2v_generate_rmat(int scale, int64_t edge_factor, const void *pcg, double a, double b,
+                          double c, int64_t chunk, void *edges_out);
+/* Symmetric CSR (ascending rows) of a sorted unique u < v edge list
+ * (Graph.csr_arrays; state.py:89-105 builds it with scipy). Host memory. */
+int s2v_build_csr(int64_t n, const int64_t *edges, int64_t E, int64_t *row_ptr, int32_t *cols);
 
 /* ---- collectives (replaces collective.py's in-process Comm) -------------- */
 int s2v_comm_unique_id(void *out, size_t len);

@@ -18,6 +18,7 @@ S2V_OK, S2V_EINVAL, S2V_EACTION, S2V_ECOMM, S2V_ECUDA, S2V_ENONFINITE = range(6)
 S2V_F32, S2V_F64 = 0, 1
 KEY_BYTES = 16  # struct Key {uint64 s; uint64 inv;}
 TOPK_MAX = 8
+HUB_DEGREE = 4096  # include/s2v.h S2V_HUB_DEGREE
 
 
 class s2v_shard(ctypes.Structure):
@@ -41,6 +42,7 @@ class s2v_shard(ctypes.Structure):
         ("cand", ctypes.c_void_p),
         ("residual", ctypes.c_void_p),
         ("order", ctypes.c_void_p),
+        ("n_hub", ctypes.c_int64),
     ]
 
 
@@ -81,6 +83,8 @@ _SIGNATURES = {
     "s2v_comm_allreduce": ([_P, _P, _SZ, _I, _P], _I),
     "s2v_memcpy_async": ([_P, _P, _SZ, _P], _I),
     "s2v_generate_ba": ([_I64, _I64, _P, _P], _I64),
+    "s2v_generate_rmat": ([_I, _I64, _P, _D, _D, _D, _I64, _P], _I64),
+    "s2v_build_csr": ([_I64, _P, _I64, _P, _P], _I),
 }
 
 _lib = None

@@ -544,7 +544,8 @@ __global__ void __launch_bounds__(256) gather64_kernel(s2v_shard sh,
   const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
   const int64_t nhw = ((int64_t)gridDim.x * blockDim.x) >> 4;
-  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + tid) >> 4; q < nrows; q += nhw) {
+  const int64_t first = sh.order ? sh.n_hub : 0;  // hub rows: hub_gather64_kernel
+  for (int64_t q = first + (((int64_t)blockIdx.x * blockDim.x + tid) >> 4); q < nrows; q += nhw) {
     const int64_t r = sh.order ? sh.order[q] : q;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (!sh.sol[r])
@@ -552,6 +553,62 @@ __global__ void __launch_bounds__(256) gather64_kernel(s2v_shard sh,
                          hot_rows, pol_hot, pol_cold);
     st4(out + r * 64 + 4 * sub, acc);
   }
+}
+
+// spmm_t of the hub rows: one CTA per row, cooperative gather.
+__global__ void __launch_bounds__(256, 1) hub_gather64_kernel(s2v_shard sh,
+                                                              const float *__restrict__ src,
+                                                              float *__restrict__ out,
+                                                              int *__restrict__ counter,
+                                                              uint32_t hot_rows) {
+  extern __shared__ __align__(16) float hub_smem[];
+  __shared__ int s_q;
+  const int tid = threadIdx.x, sub = tid & 15;
+  const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_q = atomicAdd(counter, 1);
+    __syncthreads();
+    const int64_t q = s_q;
+    if (q >= sh.n_hub) break;
+    const int64_t r = sh.order[q];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!sh.sol[r])
+      acc = hub_gather_row64(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, src, hub_smem, hot_rows,
+                             pol_hot, pol_cold);
+    if (tid < 16) st4(out + r * 64 + sub * 4, acc);
+  }
+}
+
+static int hub_gather_launch(const s2v_shard *sh, const float *src, float *out,
+                             uint32_t hot_rows, cudaStream_t st, cudaStream_t *side,
+                             cudaEvent_t *done) {
+  static thread_local cudaStream_t hs = nullptr;
+  static thread_local cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  static thread_local int *counter = nullptr;
+  static thread_local int dev_of = -1;
+  int dev = 0;
+  S2V_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev_of != dev) {
+    S2V_CUDA_CHECK(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+    S2V_CUDA_CHECK(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+    S2V_CUDA_CHECK(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+    S2V_CUDA_CHECK(cudaMalloc(&counter, sizeof(int)));
+    dev_of = dev;
+  }
+  const size_t smem = sizeof(float) * 2 * kHubBatch * 64;
+  S2V_CUDA_CHECK(cudaFuncSetAttribute(hub_gather64_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  S2V_CUDA_CHECK(cudaEventRecord(ev_ready, st));
+  S2V_CUDA_CHECK(cudaStreamWaitEvent(hs, ev_ready, 0));
+  S2V_CUDA_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), hs));
+  int grid = (int)std::min<int64_t>(sh->n_hub, kNumSMs);
+  hub_gather64_kernel<<<grid, 256, smem, hs>>>(*sh, src, out, counter, hot_rows);
+  S2V_LAUNCH_CHECK();
+  S2V_CUDA_CHECK(cudaEventRecord(ev_done, hs));
+  *side = hs;
+  *done = ev_done;
+  return S2V_OK;
 }
 
 template <class T>
@@ -618,9 +675,16 @@ int s2v_gather(s2v_dtype dt, const s2v_shard *sh, int K, const void *src, void *
   int64_t rows = (int64_t)sh->batch * sh->num_rows;
   if (rows == 0) return S2V_OK;
   if (dt == S2V_F32 && K == 64) {
-    gather64_kernel<<<kNumSMs * 8, 256, 0, as_stream(stream)>>>(
-        *sh, (const float *)src, (float *)out, (uint32_t)((48ull << 20) / 256));
+    const uint32_t hot = (uint32_t)((48ull << 20) / 256);
+    cudaStream_t st = as_stream(stream), side = nullptr;
+    cudaEvent_t done = nullptr;
+    if (sh->order && sh->n_hub > 0) {
+      int rc = hub_gather_launch(sh, (const float *)src, (float *)out, hot, st, &side, &done);
+      if (rc) return rc;
+    }
+    gather64_kernel<<<kNumSMs * 8, 256, 0, st>>>(*sh, (const float *)src, (float *)out, hot);
     S2V_LAUNCH_CHECK();
+    if (done) S2V_CUDA_CHECK(cudaStreamWaitEvent(st, done, 0));
     return S2V_OK;
   }
   int grid = (int)std::min<int64_t>((rows * 32 + 255) / 256, kNumSMs * 16);

@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
   const int hbase = tid & 16;
   const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
-  const int64_t ntiles = (nrows + kTileRows - 1) / kTileRows;
+  const int64_t first = sh.order ? sh.n_hub : 0;  // hub rows: hub_round64_kernel
+  const int64_t ntiles = (nrows - first + kTileRows - 1) / kTileRows;
   for (;;) {
     __syncthreads();
     if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
     if (tid < kTileRows) {
-      const int64_t q = tile * kTileRows + tid;
+      const int64_t q = first + tile * kTileRows + tid;
       s_rows[tid] = q < nrows ? (sh.order ? sh.order[q] : (int32_t)q) : -1;
     }
     __syncthreads();
@@ -205,6 +206,94 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
     }
   }
 }
+
+// One CTA per hub row (the first sh.n_hub rows of sh.order): cooperative
+// gather (hub_gather_row64), then the same e12 + theta4 chain + relu epilogue
+// computed by 64 threads.  Runs on a side stream concurrently with
+// round64_kernel, which handles every other row.
+__global__ void __launch_bounds__(256, 1) hub_round64_kernel(
+    s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ table, int max_deg,
+    const float *__restrict__ h_in, float *__restrict__ h_out, float *__restrict__ m_out,
+    int *__restrict__ counter, uint32_t hot_rows) {
+  extern __shared__ __align__(16) float hub_smem[];
+  float *ring = hub_smem;                              // [2][120][64]
+  float(*thT)[65] = reinterpret_cast<float(*)[65]>(hub_smem + 2 * kHubBatch * 64);
+  float *mrow = hub_smem + 2 * kHubBatch * 64 + 64 * 65;
+  __shared__ int s_q;
+  const int tid = threadIdx.x, sub = tid & 15;
+  for (int idx = tid; idx < 64 * 64; idx += 256) thT[idx % 64][idx / 64] = theta4[idx];
+  const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_q = atomicAdd(counter, 1);
+    __syncthreads();
+    const int64_t q = s_q;
+    if (q >= sh.n_hub) break;
+    const int64_t r = sh.order[q];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (h_in && !sh.sol[r])
+      acc = hub_gather_row64(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, h_in, ring, hot_rows,
+                             pol_hot, pol_cold);
+    if (tid < 16) {
+      *reinterpret_cast<float4 *>(mrow + sub * 4) = acc;
+      if (m_out) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
+    }
+    __syncthreads();
+    if (tid < 64) {
+      float z = 0.f;
+      for (int p = 0; p < 64; p++) z = __fmaf_rn(thT[p][tid], mrow[p], z);
+      const int64_t b = r / sh.num_rows, i = r - b * sh.num_rows;
+      const int trow = sh.sol[r] ? max_deg + 1 : sh.rdeg[r];
+      const int64_t phys = (b * sh.world + sh.rank) * sh.rows_max + i;
+      h_out[phys * 64 + tid] = relu(__fadd_rn(table[(int64_t)trow * 64 + tid], z));
+    }
+  }
+}
+
+// side stream + events for the hub kernels (per thread / device)
+struct SideStream {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ready = nullptr, done = nullptr;
+  int *counter = nullptr;
+  int device = -1;
+};
+
+static int side_stream(SideStream **out) {
+  static thread_local SideStream ss;
+  int dev = 0;
+  S2V_CUDA_CHECK(cudaGetDevice(&dev));
+  if (ss.device != dev) {
+    S2V_CUDA_CHECK(cudaStreamCreateWithFlags(&ss.stream, cudaStreamNonBlocking));
+    S2V_CUDA_CHECK(cudaEventCreateWithFlags(&ss.ready, cudaEventDisableTiming));
+    S2V_CUDA_CHECK(cudaEventCreateWithFlags(&ss.done, cudaEventDisableTiming));
+    S2V_CUDA_CHECK(cudaMalloc(&ss.counter, sizeof(int)));
+    ss.device = dev;
+  }
+  *out = &ss;
+  return S2V_OK;
+}
+
+// Launch `launch_hub(side_stream, counter)` concurrently with the work the
+// caller enqueues next on `st`; returns after making `st` wait for it.
+template <class F>
+static int with_hub_kernel(const s2v_shard *sh, cudaStream_t st, F launch_hub,
+                           SideStream **ss_out) {
+  *ss_out = nullptr;
+  if (!sh->order || sh->n_hub <= 0) return S2V_OK;
+  SideStream *ss = nullptr;
+  int rc = side_stream(&ss);
+  if (rc) return rc;
+  S2V_CUDA_CHECK(cudaEventRecord(ss->ready, st));
+  S2V_CUDA_CHECK(cudaStreamWaitEvent(ss->stream, ss->ready, 0));
+  S2V_CUDA_CHECK(cudaMemsetAsync(ss->counter, 0, sizeof(int), ss->stream));
+  launch_hub(ss->stream, ss->counter);
+  S2V_LAUNCH_CHECK();
+  S2V_CUDA_CHECK(cudaEventRecord(ss->done, ss->stream));
+  *ss_out = ss;
+  return S2V_OK;
+}
+
+constexpr size_t kHubSmem = sizeof(float) * (2 * kHubBatch * 64 + 64 * 65 + 64);
 
 // ---------------------------------------------------------------------------
 // numpy pairwise column sums over the N nodes of each slot (policy.py:199).
@@ -673,9 +762,22 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
       return (uint32_t)(e ? atoi(e) : 48);
     }();
     hot_rows = (uint32_t)(((uint64_t)hot_env << 20) / 256);
+    SideStream *ss = nullptr;
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(hub_round64_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kHubSmem));
+    int rc = with_hub_kernel(sh, st, [&](cudaStream_t hs, int *hub_counter) {
+      int hgrid = (int)std::min<int64_t>(sh->n_hub, kNumSMs);
+      hub_round64_kernel<<<hgrid, 256, kHubSmem, hs>>>(
+          *sh, (const float *)theta4, (const float *)table, max_deg, (const float *)h_in,
+          (float *)h_out, (float *)m_out, hub_counter, hot_rows);
+    }, &ss);
+    if (rc) return rc;
     round64_kernel<<<grid, 256, 0, st>>>(*sh, (const float *)theta4, (const float *)table,
                                          max_deg, (const float *)h_in, (float *)h_out,
                                          (float *)m_out, counter, hot_rows);
+    S2V_LAUNCH_CHECK();
+    if (ss) S2V_CUDA_CHECK(cudaStreamWaitEvent(st, ss->done, 0));
     S2V_LAUNCH_CHECK();
     return S2V_OK;
   }

@@ -82,4 +82,63 @@ __device__ __forceinline__ float4 gather_row64(int64_t e, const int64_t e1,
 }
 
 
+// CTA-cooperative sequential gather of one hub row (degree > S2V_HUB_DEGREE):
+// half-warps 1..15 stage 8 neighbour rows each (kHubBatch = 120 per batch)
+// into a double-buffered shared ring while half-warp 0 adds the previous
+// batch in ascending order, so one chain gets 120 rows in flight instead of
+// 8.  Removed entries are staged as +0 (value-equal to skipping them, as the
+// reference adds 0 * h).  The result is valid in half-warp 0.
+constexpr int kHubLoaders = 15;
+constexpr int kHubBatch = kHubLoaders * 8;
+
+__device__ __forceinline__ void hub_stage(int64_t e_batch, const int64_t e1,
+                                          const uint32_t *__restrict__ cols,
+                                          const float *__restrict__ src, float *buf /*[120][64]*/,
+                                          int hw, int sub, unsigned hmask, int hbase,
+                                          uint32_t hot_rows, uint64_t pol_hot, uint64_t pol_cold) {
+  if (hw == 0) return;
+  const int64_t base = e_batch + (int64_t)(hw - 1) * 8;
+  const uint32_t mine = (sub < 8 && base + sub < e1) ? ldg_u32_pol(cols + base + sub, pol_cold)
+                                                     : S2V_DEAD;
+  float4 v[8];
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    const uint32_t c = __shfl_sync(hmask, mine, hbase + q);
+    v[q] = (c & S2V_DEAD) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                          : ldg_f4_pol(src + (int64_t)c * 64 + sub * 4,
+                                       c < hot_rows ? pol_hot : pol_cold);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; q++)
+    *reinterpret_cast<float4 *>(buf + ((hw - 1) * 8 + q) * 64 + sub * 4) = v[q];
+}
+
+__device__ __forceinline__ float4 hub_gather_row64(const int64_t e0, const int64_t e1,
+                                                   const uint32_t *__restrict__ cols,
+                                                   const float *__restrict__ src,
+                                                   float *ring /*[2][120][64]*/, uint32_t hot_rows,
+                                                   uint64_t pol_hot, uint64_t pol_cold) {
+  const int tid = threadIdx.x, hw = tid >> 4, sub = tid & 15;
+  const unsigned hmask = (tid & 16) ? 0xFFFF0000u : 0x0000FFFFu;
+  const int hbase = tid & 16;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t nb = (e1 - e0 + kHubBatch - 1) / kHubBatch;
+  if (nb > 0)
+    hub_stage(e0, e1, cols, src, ring, hw, sub, hmask, hbase, hot_rows, pol_hot, pol_cold);
+  __syncthreads();
+  for (int64_t b = 0; b < nb; b++) {
+    if (b + 1 < nb)
+      hub_stage(e0 + (b + 1) * kHubBatch, e1, cols, src, ring + ((b + 1) & 1) * kHubBatch * 64, hw,
+                sub, hmask, hbase, hot_rows, pol_hot, pol_cold);
+    if (hw == 0) {
+      const float *cur = ring + (b & 1) * kHubBatch * 64;
+      const int64_t left = e1 - e0 - b * kHubBatch;
+      const int cnt = left < kHubBatch ? (int)left : kHubBatch;
+      for (int q = 0; q < cnt; q++) add4(acc, *reinterpret_cast<const float4 *>(cur + q * 64 + sub * 4));
+    }
+    __syncthreads();
+  }
+  return acc;
+}
+
 }  // namespace s2v

@@ -96,9 +96,12 @@ class _ShardStructure:
         self.nnz = hi - lo
         self.rows = rows
         self.max_deg = int(np.diff(row_ptr).max()) if rows else 0
-        # descending-degree processing order (load balance of the round kernel)
-        self.order = to_device(np.argsort(-np.diff(row_ptr), kind="stable").astype(np.int32),
-                               device)
+        # descending-degree processing order (load balance of the round
+        # kernel); rows above the hub degree go to the CTA-cooperative kernel
+        deg = np.diff(row_ptr)
+        by_degree = np.argsort(-deg, kind="stable").astype(np.int32)
+        self.n_hub = int(np.count_nonzero(deg > _lib.HUB_DEGREE))
+        self.order = to_device(by_degree, device)
         self.row_ptr = to_device(row_ptr, device)
         self.cols0 = to_device(cols0, device)
         self.col_ptr = to_device(col_ptr, device)
@@ -167,8 +170,14 @@ class PartitionedState:
             if self.nnz else torch.zeros(1, dtype=torch.int64, device=dev)
         self.col_row = torch.cat([s.col_row + int(b * rows) for b, s in enumerate(structs)]) \
             if self.nnz else torch.zeros(1, dtype=torch.int32, device=dev)
-        self.order = torch.cat([s.order + int(b * rows) for b, s in enumerate(structs)]) \
-            if rows else torch.zeros(1, dtype=torch.int32, device=dev)
+        # hub rows of every slot first, then the remaining rows of every slot
+        if rows:
+            self.order = torch.cat(
+                [s.order[:s.n_hub] + int(b * rows) for b, s in enumerate(structs)] +
+                [s.order[s.n_hub:] + int(b * rows) for b, s in enumerate(structs)])
+        else:
+            self.order = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.n_hub = sum(s.n_hub for s in structs)
         nr = max(batch * rows, 1)
         self.rdeg = torch.zeros(nr, dtype=torch.int32, device=dev)
         self.sol_d = torch.zeros(nr, dtype=torch.uint8, device=dev)
@@ -180,7 +189,7 @@ class PartitionedState:
             row_ptr=ptr(self.row_ptr), cols=ptr(self.cols), col_ptr=ptr(self.col_ptr),
             col_ent=ptr(self.col_ent), col_row=ptr(self.col_row), rdeg=ptr(self.rdeg),
             sol=ptr(self.sol_d), cand=ptr(self.cand_d), residual=ptr(self.residual_d),
-            order=ptr(self.order))
+            order=ptr(self.order), n_hub=self.n_hub)
         sol_phys = np.zeros((batch, P, self.rows_max), dtype=np.uint8)
         if P == 1:
             sol_phys[:, 0, :] = solutions

@@ -39,3 +39,25 @@ def test_forward_bitwise_vs_oracle(n, m, K, L, seed, solfrac, dtype):
     assert np.array_equal(cand_gpu, cand)
     assert np.array_equal(h_gpu, h), np.abs(h_gpu - h).max()
     assert np.array_equal(s_gpu, sc), np.abs(s_gpu - sc).max()
+
+
+def _hub_graph():
+    """BA(3000,4) plus a star: node 7 joined to 5000 others, so node 7 (and
+    nothing else) exceeds the hub degree and takes the cooperative kernel."""
+    base = P.generate_ba(6000, 4, 5)
+    extra = np.stack([np.full(5000, 7), np.arange(1000, 6000)], axis=1)
+    return P.Graph(6000, np.concatenate([base.edge_array, extra]))
+
+
+@pytest.mark.parametrize("make", ["hub", "rmat16"])
+def test_hub_rows_bitwise_vs_oracle(make):
+    g = _hub_graph() if make == "hub" else P.generate_rmat(16, 16, 0)
+    rp, cols = g.csr_arrays()
+    assert np.diff(rp).max() > 4096
+    params = P.PolicyParams.initialize(64, 5, seed=1)
+    sol = (np.random.default_rng(2).random(g.num_nodes) < 0.05).astype(np.uint8)
+    h_gpu, s_gpu, cand_gpu = _forward_gpu(g, params, sol)
+    h, _, _, cand, sc = cref.forward(rp, cols, sol, params.as_dict(), 5)
+    assert np.array_equal(cand_gpu, cand)
+    assert np.array_equal(h_gpu, h)
+    assert np.array_equal(s_gpu, sc)

@@ -92,3 +92,27 @@ def test_adam_bitwise_vs_port():
     for k in P.PARAM_NAMES:
         assert np.array_equal(getattr(params, k), theta[k]), k
         assert np.array_equal(adam.m[k], m[k]) and np.array_equal(adam.v[k], v[k])
+
+
+def test_loss_and_gradients_with_hub_rows_vs_port():
+    base = P.generate_ba(6000, 4, 5)
+    extra = np.stack([np.full(5000, 7), np.arange(1000, 6000)], axis=1)
+    g = P.Graph(6000, np.concatenate([base.edge_array, extra]))
+    rng = np.random.default_rng(3)
+    B, n = 2, 6000
+    sols = (rng.random((B, n)) < 0.05).astype(np.uint8)
+    sols[:, 7] = 0
+    params = P.PolicyParams.initialize(64, 4, seed=5, orientation="symmetric")
+    ps = port.ResidualState([g.edge_array] * B, n, solutions=sols)
+    actions = np.array([7, int(np.flatnonzero(ps.cand[1])[3])])
+    targets = rng.normal(size=B).astype(np.float32)
+
+    def worker(comm):
+        st = P.PartitionedState([g] * B, P.partition_rows(n, 1)[0], solutions=sols)
+        assert st.n_hub >= 1
+        return P.loss_and_gradients(st, actions, targets, params, comm)
+    loss, grads = P.run_workers(1, worker)[0]
+    loss_o, grads_o = port.loss_and_grads(ps, actions, targets, params.as_dict(), 4)
+    assert abs(loss - loss_o) <= 1e-4 * max(1.0, abs(loss_o))
+    for k in P.PARAM_NAMES:
+        assert scale_error(grads[k], grads_o[k]).max() < 1e-4, k
