@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--train-steps", type=int, default=5)
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg1 / cfg5 legs")
+    ap.add_argument("--rmat-scale", type=int, default=22)
+    ap.add_argument("--same-device", action="store_true",
+                    help="bind every rank to cuda:0 (multi-process test on one GPU)")
     return ap.parse_args()
 
 
@@ -253,6 +257,52 @@ def cpu_train_sample(dataset, B_sample, B, tau):
 
 
 # ---------------------------------------------------------------------------
+# other inference configs: cfg1 (launch-bound small graph) and cfg5 (R-MAT)
+# ---------------------------------------------------------------------------
+
+
+def infer_leg(P, comm, graph, steps, warmup, name):
+    """Device time per inference step (solve_step) walking an episode from
+    S = {}; stops early if the episode ends."""
+    import torch
+    from paper_2105_08764_b200.inference import solve_step
+    part = P.partition_rows(graph.num_nodes, comm.size)[comm.rank]
+    params = P.PolicyParams.initialize(64, 5, seed=0)
+    sched = P.SelectionSchedule.adaptive()
+    state = P.PartitionedState([graph], part)
+    active = np.array([True])
+    for _ in range(warmup):
+        solve_step(state, params, comm, sched, active)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    done = 0
+    for _ in range(steps):
+        if int(state.local_residual.sum()) == 0:
+            break
+        solve_step(state, params, comm, sched, active)
+        done += 1
+    e1.record()
+    torch.cuda.synchronize()
+    rp, _ = graph.csr_arrays()
+    deg = np.diff(rp)
+    return {"workload": name, "value": e0.elapsed_time(e1) / max(done, 1) / 1e3, "unit": "s",
+            "steps": done, "warmup": warmup, "nodes": graph.num_nodes,
+            "edges": graph.num_edges, "max_degree": int(deg.max()),
+            "hub_rows": int(state.n_hub), "isolated_frac": float(np.mean(deg == 0))}
+
+
+def full_solve_leg(P, comm, graph):
+    import torch
+    params = P.PolicyParams.initialize(64, 5, seed=0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    (res,) = P.solve([graph], params, comm)
+    torch.cuda.synchronize()
+    return time.perf_counter() - t0, res
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 
@@ -270,24 +320,27 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    bind_device(local)
+    # --same-device: every rank on cuda:0 (exercises the multi-process path on
+    # a one-GPU box); otherwise one GPU per rank
+    bind_device(0 if args.same_device else local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # host-side plumbing only (barrier, timing max, small host exchanges);
+        # the halo data path is the IPC peer-memory transport (DistComm)
+        dist.init_process_group("gloo")
         comm = P.DistComm()
     else:
         comm = P.WorkerGroup(1).comm(0)
 
     def barrier():
         if world > 1:
-            torch.distributed.barrier()
+            torch.cuda.synchronize()
+            comm.barrier()
 
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+        return float(max(comm.all_gather(np.array([x], np.float64), tag="bench")))
 
     t0 = time.time()
     graph = P.generate_ba(args.nodes, args.m, 0)
@@ -396,6 +449,37 @@ def main():
                          "(node-level batch), K=64, T=5, tau=4 (BASELINE configs[3])")
         train.append(leg4)
 
+    extra = None
+    if not args.no_extra:
+        extra = []
+        g1 = P.generate_ba(1000, 4, 0)
+        leg1 = infer_leg(P, comm, g1, 50, 5, "MVC inference step, BA(1000,4,seed=0), K=64, T=5 "
+                                            "(BASELINE configs[0]; launch-bound)")
+        t_solve, res = full_solve_leg(P, comm, g1)
+        leg1["full_adaptive_solve_s"] = t_solve
+        leg1["full_solve_cover"] = res.cover_size
+        leg1["full_solve_evals"] = res.policy_evals
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            from oracle import port
+            theta = P.PolicyParams.initialize(64, 5, seed=0).as_dict()
+            t0 = time.perf_counter()
+            (cover, evals, _, _), = port.solve([g1.edge_array], 1000, theta, 5)
+            dt = time.perf_counter() - t0
+            leg1["cpu_baseline"] = {"value": dt / evals, "unit": "s", "cores": os.cpu_count(),
+                                    "kind": "port", "full_adaptive_solve_s": dt,
+                                    "sample": f"oracle/port.py full adaptive solve ({evals} evals,"
+                                              f" cover {len(cover)}) / evals"}
+        extra.append(leg1)
+        t0 = time.time()
+        g5 = P.generate_rmat(args.rmat_scale, 16, 0)
+        g5.csr_arrays()
+        leg5 = infer_leg(P, comm, g5, 8, 2,
+                         f"MVC inference step, R-MAT scale {args.rmat_scale} edge factor 16 "
+                         "(a,b,c = .57,.19,.19, seed 0), K=64, T=5, first steps of the adaptive "
+                         "episode (BASELINE configs[4])")
+        leg5["graph_gen_s"] = round(time.time() - t0, 2)
+        extra.append(leg5)
+
     if rank == 0:
         line = {"metric": METRIC, "value": step_ms / 1e3, "unit": "s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
@@ -404,6 +488,7 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks.summary(),
                 "train_steps": train,
+                "other_inference": extra,
                 "setup": {"graph_gen_s": round(t_gen, 2), "state_build_s": round(t_state, 3),
                           "alive_entries_at_start": alive_entries}}
         print(json.dumps(line), flush=True)

@@ -120,6 +120,13 @@ int s2v_e12_table(s2v_dtype dt, const void *theta1, const void *theta2, const vo
 int s2v_embed_round(s2v_dtype dt, const s2v_shard *sh, const void *theta4, const void *table,
                     int K, int max_deg, const void *h_in, void *h_out, void *m_out,
                     void *stream);
+/* Same round with the halo exchange fused in: every output row is also
+ * stored into each of the npeers buffers peer_outs[q] (a device array of
+ * IPC-mapped peer pointers, own buffer included) over NVLink, replacing the
+ * per-round all-gather.  K = 64 fp32. */
+int s2v_embed_round_peers(s2v_dtype dt, const s2v_shard *sh, const void *theta4,
+                          const void *table, int K, int max_deg, const void *h_in, void *h_out,
+                          void *const *peer_outs, int npeers, void *m_out, void *stream);
 
 /* g[b][k] = numpy pairwise sum over the N nodes of slot b of h[.,k]; h must
  * hold every rank's rows (after an all-gather when P>1).  Replaces
@@ -211,6 +218,14 @@ int s2v_comm_allreduce(void *comm, void *buf, size_t count, int kind /*0 i64 1 f
  * transport (ranks as threads, possibly sharing one device) moves halo chunks
  * with peer copies instead of NCCL. */
 int s2v_memcpy_async(void *dst, const void *src, size_t bytes, void *stream);
+/* Peer-memory transport for process ranks: IPC export/import of device
+ * allocations (handle_out: 64 bytes; offset of ptr inside its allocation) and
+ * stream-ordered flags (write a value after prior work / wait until >=). */
+int s2v_ipc_export(const void *ptr, void *handle_out, uint64_t *offset_out);
+int s2v_ipc_import(const void *handle, void **base_out);
+int s2v_ipc_close(void *base);
+int s2v_stream_write_u32(void *addr, uint32_t value, void *stream);
+int s2v_stream_wait_u32(void *addr, uint32_t value, void *stream);
 
 #ifdef __cplusplus
 }

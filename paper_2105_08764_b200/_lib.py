@@ -62,6 +62,7 @@ _SIGNATURES = {
     "s2v_apply_phase2": ([_SH, _P, _I, _P, _P, _P, _P], _I),
     "s2v_e12_table": ([_I, _P, _P, _P, _I, _I, _P, _P], _I),
     "s2v_embed_round": ([_I, _SH, _P, _P, _I, _I, _P, _P, _P, _P], _I),
+    "s2v_embed_round_peers": ([_I, _SH, _P, _P, _I, _I, _P, _P, _P, _I, _P, _P], _I),
     "s2v_colsum": ([_I, _SH, _I, _P, _P, _P, _SZ, _P], _I),
     "s2v_colsum_workspace": ([_SH, _I, _I], _SZ),
     "s2v_score": ([_I, _SH, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P], _I),
@@ -82,6 +83,11 @@ _SIGNATURES = {
     "s2v_comm_allgather_slots": ([_P, _P, _SZ, _SZ, _I, _I, _P], _I),
     "s2v_comm_allreduce": ([_P, _P, _SZ, _I, _P], _I),
     "s2v_memcpy_async": ([_P, _P, _SZ, _P], _I),
+    "s2v_ipc_export": ([_P, _P, ctypes.POINTER(ctypes.c_uint64)], _I),
+    "s2v_ipc_import": ([_P, ctypes.POINTER(ctypes.c_void_p)], _I),
+    "s2v_ipc_close": ([_P], _I),
+    "s2v_stream_write_u32": ([_P, ctypes.c_uint32, _P], _I),
+    "s2v_stream_wait_u32": ([_P, ctypes.c_uint32, _P], _I),
     "s2v_generate_ba": ([_I64, _I64, _P, _P], _I64),
     "s2v_generate_rmat": ([_I, _I64, _P, _D, _D, _D, _I64, _P], _I64),
     "s2v_build_csr": ([_I64, _P, _I64, _P, _P], _I),
@@ -134,7 +140,7 @@ def check(rc: int, what: str = "") -> None:
 # kernels each entry point launches (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {
     "s2v_shard_init": 1, "s2v_apply_phase1": 1, "s2v_apply_phase2": 2, "s2v_e12_table": 1,
-    "s2v_embed_round": 1, "s2v_colsum": 2, "s2v_score": 1, "s2v_topk_merge": 1,
+    "s2v_embed_round": 1, "s2v_embed_round_peers": 1, "s2v_colsum": 2, "s2v_score": 1, "s2v_topk_merge": 1,
     "s2v_grad_h_init": 1, "s2v_layer_backward": 1, "s2v_gather": 1, "s2v_param_grads": 1,
     "s2v_reduce_partials": 1, "s2v_head_backward": 1, "s2v_adam": 1,
 }

@@ -110,9 +110,11 @@ class _DeviceComm:
         self.handle = handle
         self.world, self.rank = world, rank
 
-    def allgather_slots(self, buf_ptr: int, chunk_bytes: int, slot_stride: int, nslots: int,
-                        stream: int) -> None:
-        self._lib.call("s2v_comm_allgather_slots", self.handle, buf_ptr, chunk_bytes,
+    supports_push = False
+
+    def allgather_rows(self, tensor, chunk_bytes: int, slot_stride: int, nslots: int,
+                       stream: int, peers=None) -> None:
+        self._lib.call("s2v_comm_allgather_slots", self.handle, tensor.data_ptr(), chunk_bytes,
                        slot_stride, nslots, self.rank, stream)
 
     def allreduce(self, buf_ptr: int, count: int, kind: int, stream: int) -> None:
@@ -143,6 +145,12 @@ class _LocalDeviceComm:
     def _publish(self, value):
         return self.comm.group._exchange_objects(self.rank, value)
 
+    supports_push = False
+
+    def allgather_rows(self, tensor, chunk_bytes: int, slot_stride: int, nslots: int,
+                       stream: int, peers=None) -> None:
+        self.allgather_slots(tensor.data_ptr(), chunk_bytes, slot_stride, nslots, stream)
+
     def allgather_slots(self, buf_ptr: int, chunk_bytes: int, slot_stride: int, nslots: int,
                         stream: int) -> None:
         import torch
@@ -164,20 +172,113 @@ class _LocalDeviceComm:
                 torch.cuda.current_stream().wait_event(ev)
 
     def allreduce(self, buf_ptr: int, count: int, kind: int, stream: int) -> None:
-        import torch
-        dt = {0: torch.int64, 1: torch.float64, 2: torch.float32}[kind]
-        host = torch.empty(count, dtype=dt)
-        self._lib.call("s2v_memcpy_async", host.data_ptr(), buf_ptr, count * host.element_size(),
-                       stream)
-        torch.cuda.current_stream().synchronize()
-        total = self.comm.all_reduce_sum(host.numpy().copy(), tag="device")
-        host.copy_(torch.from_numpy(np.ascontiguousarray(total, dtype=host.numpy().dtype)))
-        self._lib.call("s2v_memcpy_async", buf_ptr, host.data_ptr(), count * host.element_size(),
-                       stream)
-        torch.cuda.current_stream().synchronize()
+        _host_allreduce(self._lib, self.comm, buf_ptr, count, kind, stream)
 
     def close(self) -> None:
         pass
+
+
+class _IpcDeviceComm:
+    """Peer-memory transport for process ranks (torchrun / DistComm).
+
+    Halo buffers are mapped into every peer with CUDA IPC; the forward round
+    kernel pushes each output row into all peers' buffers itself
+    (s2v_embed_round_peers -- the exchange is fused into the compute), and
+    ranks order producer/consumer through per-peer flags written and waited
+    on by the CUDA streams (no host barrier, no SM spinning).  Ranks may
+    share a GPU (tests) or own one each (NVLink P2P).  Generic layouts fall
+    back to pulling peers' chunks with copies between two flag epochs.
+    """
+
+    supports_push = True
+
+    def __init__(self, comm: "DistComm"):
+        import torch
+        from . import _lib
+        self._lib = _lib
+        self.comm = comm
+        self.world, self.rank = comm.size, comm.rank
+        self._imports: dict[bytes, int] = {}
+        self.epoch = 0
+        self.flags = torch.zeros(max(self.world, 1) * 8, dtype=torch.int32, device="cuda")
+        self.peer_flags = self.peers_of(self.flags)
+
+    def _export(self, ptr: int):
+        handle = ctypes.create_string_buffer(64)
+        off = ctypes.c_uint64()
+        self._lib.call("s2v_ipc_export", ptr, handle, ctypes.byref(off))
+        return handle.raw, int(off.value)
+
+    def _import(self, handle: bytes) -> int:
+        base = self._imports.get(handle)
+        if base is None:
+            out = ctypes.c_void_p()
+            self._lib.call("s2v_ipc_import", ctypes.create_string_buffer(handle, 64),
+                           ctypes.byref(out))
+            base = int(out.value)
+            self._imports[handle] = base
+        return base
+
+    def peers_of(self, tensor) -> list[int]:
+        """Every rank's address of the same-role buffer (own included).
+
+        Collective: every rank must register its same-role buffer at the same
+        point (callers cache the result per workspace, never by address --
+        allocator address reuse differs across ranks)."""
+        handle, off = self._export(tensor.data_ptr())
+        allh = self.comm._gather_objects((handle, off))
+        return [tensor.data_ptr() if q == self.rank else self._import(h) + o
+                for q, (h, o) in enumerate(allh)]
+
+    def peer_array(self, tensor):
+        """peers_of as a device array of pointers (kernel argument)."""
+        import torch
+        return torch.tensor(self.peers_of(tensor), dtype=torch.int64, device=tensor.device)
+
+    def signal_and_wait(self, stream: int) -> None:
+        """Stream-ordered all-rank barrier: after this rank's prior work, raise
+        its flag in every peer; before later work, wait for every peer's."""
+        self.epoch += 1
+        for q in range(self.world):
+            self._lib.call("s2v_stream_write_u32", self.peer_flags[q] + 4 * self.rank,
+                           self.epoch, stream)
+        own = self.flags.data_ptr()
+        for q in range(self.world):
+            self._lib.call("s2v_stream_wait_u32", own + 4 * q, self.epoch, stream)
+
+    def allgather_rows(self, tensor, chunk_bytes: int, slot_stride: int, nslots: int,
+                       stream: int, peers=None) -> None:
+        if peers is None:
+            raise ValueError("IPC all-gather needs the buffer's registered peer list")
+        self.signal_and_wait(stream)  # every producer is done
+        own = tensor.data_ptr()
+        for q in range(self.world):
+            if q == self.rank:
+                continue
+            for b in range(nslots):
+                off = b * slot_stride + q * chunk_bytes
+                self._lib.call("s2v_memcpy_async", own + off, peers[q] + off, chunk_bytes, stream)
+        self.signal_and_wait(stream)  # every reader is done before buffers are reused
+
+    def allreduce(self, buf_ptr: int, count: int, kind: int, stream: int) -> None:
+        _host_allreduce(self._lib, self.comm, buf_ptr, count, kind, stream)
+
+    def close(self) -> None:
+        for base in self._imports.values():
+            self._lib.load().s2v_ipc_close(base)
+        self._imports.clear()
+
+
+def _host_allreduce(lib, comm, buf_ptr: int, count: int, kind: int, stream: int) -> None:
+    import torch
+    dt = {0: torch.int64, 1: torch.float64, 2: torch.float32}[kind]
+    host = torch.empty(count, dtype=dt)
+    lib.call("s2v_memcpy_async", host.data_ptr(), buf_ptr, count * host.element_size(), stream)
+    torch.cuda.current_stream().synchronize()
+    total = comm.all_reduce_sum(host.numpy().copy(), tag="device")
+    host.copy_(torch.from_numpy(np.ascontiguousarray(total, dtype=host.numpy().dtype)))
+    lib.call("s2v_memcpy_async", buf_ptr, host.data_ptr(), count * host.element_size(), stream)
+    torch.cuda.current_stream().synchronize()
 
 
 def _new_unique_id() -> bytes:
@@ -306,12 +407,17 @@ class DistComm:
         self._dist.barrier(group=self._gloo)
 
     def device_comm(self):
+        """IPC peer-memory transport (fused halo exchange) by default;
+        S2V_TRANSPORT=nccl selects NCCL collectives instead."""
         if self.size == 1:
             return None
         if self._dev is None:
-            uid = [_new_unique_id() if self.rank == 0 else None]
-            self._dist.broadcast_object_list(uid, src=0, group=self._gloo)
-            self._dev = _DeviceComm(uid[0], self.size, self.rank)
+            if os.environ.get("S2V_TRANSPORT", "ipc") == "nccl":
+                uid = [_new_unique_id() if self.rank == 0 else None]
+                self._dist.broadcast_object_list(uid, src=0, group=self._gloo)
+                self._dev = _DeviceComm(uid[0], self.size, self.rank)
+            else:
+                self._dev = _IpcDeviceComm(self)
         return self._dev
 
 

@@ -4,11 +4,31 @@
 // per batch slot inside an NCCL group), and small all-reduces of integer
 // selection info / fp64 gradient packs.  Host-side bookkeeping collectives
 // stay in Python (torch.distributed / thread rendezvous).
+#include <cuda.h>
 #include <nccl.h>
+
+#include <mutex>
 
 #include "s2v_common.cuh"
 
 using namespace s2v;
+
+typedef CUresult (*PFN_addr_range)(CUdeviceptr *, size_t *, CUdeviceptr);
+typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+template <class F>
+static int driver_fn(const char *name, F *out) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  S2V_CUDA_CHECK(cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess)
+    return fail(S2V_ECUDA, "driver entry point %s unavailable", name);
+  *out = (F)fn;
+  return S2V_OK;
+}
 
 extern "C" {
 
@@ -59,6 +79,64 @@ int s2v_comm_allgather_slots(void *comm, void *recv, size_t bytes, size_t slot_s
   }
   ncclResult_t r = ncclGroupEnd();
   if (r != ncclSuccess) return fail(S2V_ECOMM, "ncclGroupEnd: %s", ncclGetErrorString(r));
+  return S2V_OK;
+}
+
+// ---- CUDA IPC + stream memory operations: the peer-memory transport ------
+// Ranks that are processes (torchrun) map each other's halo buffers with
+// cudaIpc* and order producer/consumer with flags written and waited on by
+// the streams themselves (cuStreamWriteValue32 / cuStreamWaitValue32, reached
+// through cudaGetDriverEntryPoint so libs2v needs no link-time libcuda).  The
+// round kernel then pushes every output row straight into every peer's
+// buffer (s2v_embed_round_peers): the halo exchange is fused into the kernel.
+int s2v_ipc_export(const void *ptr, void *handle_out, uint64_t *offset_out) {
+  static PFN_addr_range range = nullptr;
+  if (!range) {
+    int rc = driver_fn("cuMemGetAddressRange", &range);
+    if (rc) return rc;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+    return fail(S2V_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  S2V_CUDA_CHECK(cudaIpcGetMemHandle(&h, (void *)base));
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (uint64_t)((CUdeviceptr)ptr - base);
+  return S2V_OK;
+}
+
+int s2v_ipc_import(const void *handle, void **base_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  S2V_CUDA_CHECK(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return S2V_OK;
+}
+
+int s2v_ipc_close(void *base) {
+  S2V_CUDA_CHECK(cudaIpcCloseMemHandle(base));
+  return S2V_OK;
+}
+
+int s2v_stream_write_u32(void *addr, uint32_t value, void *stream) {
+  static PFN_write32 w = nullptr;
+  if (!w) {
+    int rc = driver_fn("cuStreamWriteValue32", &w);
+    if (rc) return rc;
+  }
+  if (w((CUstream)stream, (CUdeviceptr)addr, value, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+    return fail(S2V_ECOMM, "cuStreamWriteValue32 failed");
+  return S2V_OK;
+}
+
+int s2v_stream_wait_u32(void *addr, uint32_t value, void *stream) {
+  static PFN_wait32 w = nullptr;
+  if (!w) {
+    int rc = driver_fn("cuStreamWaitValue32", &w);
+    if (rc) return rc;
+  }
+  if (w((CUstream)stream, (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    return fail(S2V_ECOMM, "cuStreamWaitValue32 failed");
   return S2V_OK;
 }
 

@@ -130,7 +130,8 @@ constexpr int kTileRows = 32;
 __global__ void __launch_bounds__(256, 4) round64_kernel(
     s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ table, int max_deg,
     const float *__restrict__ h_in, float *__restrict__ h_out, float *__restrict__ m_out,
-    int *__restrict__ tile_counter, uint32_t hot_rows) {
+    int *__restrict__ tile_counter, uint32_t hot_rows, float *const *__restrict__ peers,
+    int npeers) {
   __shared__ __align__(16) float thT[64][64 + 4];        // thT[p][k] = theta4[k][p]
   __shared__ __align__(16) float ms[kTileRows][64 + 4];  // m tile
   __shared__ int32_t s_rows[kTileRows];
@@ -203,6 +204,9 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       o.w = relu(__fadd_rn(e.w, z[a][3]));
       const int64_t phys = (b * sh.world + sh.rank) * sh.rows_max + i;
       stg_f4_pol(h_out + phys * 64 + kq * 4, o, pol_cold);
+      // fused halo exchange: the same row straight into every peer's buffer
+      for (int q = 0; q < npeers; q++)
+        if (peers[q] != h_out) *reinterpret_cast<float4 *>(peers[q] + phys * 64 + kq * 4) = o;
     }
   }
 }
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
 __global__ void __launch_bounds__(256, 1) hub_round64_kernel(
     s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ table, int max_deg,
     const float *__restrict__ h_in, float *__restrict__ h_out, float *__restrict__ m_out,
-    int *__restrict__ counter, uint32_t hot_rows) {
+    int *__restrict__ counter, uint32_t hot_rows, float *const *__restrict__ peers, int npeers) {
   extern __shared__ __align__(16) float hub_smem[];
   float *ring = hub_smem;                              // [2][120][64]
   float(*thT)[65] = reinterpret_cast<float(*)[65]>(hub_smem + 2 * kHubBatch * 64);
@@ -245,7 +249,10 @@ __global__ void __launch_bounds__(256, 1) hub_round64_kernel(
       const int64_t b = r / sh.num_rows, i = r - b * sh.num_rows;
       const int trow = sh.sol[r] ? max_deg + 1 : sh.rdeg[r];
       const int64_t phys = (b * sh.world + sh.rank) * sh.rows_max + i;
-      h_out[phys * 64 + tid] = relu(__fadd_rn(table[(int64_t)trow * 64 + tid], z));
+      const float o = relu(__fadd_rn(table[(int64_t)trow * 64 + tid], z));
+      h_out[phys * 64 + tid] = o;
+      for (int q = 0; q < npeers; q++)
+        if (peers[q] != h_out) peers[q][phys * 64 + tid] = o;
     }
   }
 }
@@ -744,7 +751,7 @@ __global__ void topk_merge_kernel(const Key *__restrict__ block_keys, int nblk, 
 template <class T>
 static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *table, int K,
                          int max_deg, const void *h_in, void *h_out, void *m_out,
-                         cudaStream_t st) {
+                         cudaStream_t st, float *const *peers = nullptr, int npeers = 0) {
   const int64_t nrows = (int64_t)sh->batch * sh->num_rows;
   if (nrows == 0) return S2V_OK;
   if (sizeof(T) == 4 && K == 64) {
@@ -770,17 +777,18 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
       int hgrid = (int)std::min<int64_t>(sh->n_hub, kNumSMs);
       hub_round64_kernel<<<hgrid, 256, kHubSmem, hs>>>(
           *sh, (const float *)theta4, (const float *)table, max_deg, (const float *)h_in,
-          (float *)h_out, (float *)m_out, hub_counter, hot_rows);
+          (float *)h_out, (float *)m_out, hub_counter, hot_rows, peers, npeers);
     }, &ss);
     if (rc) return rc;
     round64_kernel<<<grid, 256, 0, st>>>(*sh, (const float *)theta4, (const float *)table,
                                          max_deg, (const float *)h_in, (float *)h_out,
-                                         (float *)m_out, counter, hot_rows);
+                                         (float *)m_out, counter, hot_rows, peers, npeers);
     S2V_LAUNCH_CHECK();
     if (ss) S2V_CUDA_CHECK(cudaStreamWaitEvent(st, ss->done, 0));
     S2V_LAUNCH_CHECK();
     return S2V_OK;
   }
+  if (npeers) return fail(S2V_EINVAL, "fused peer rounds need K = 64 fp32");
   if (K > 256) return fail(S2V_EINVAL, "embed_dim %d > 256 unsupported", K);
   size_t smem = sizeof(T) * ((size_t)K * (K + 1) + 8 * (size_t)K);
   int grid = (int)std::min<int64_t>((nrows + 7) / 8, kNumSMs * 8);
@@ -834,6 +842,15 @@ int s2v_e12_table(s2v_dtype dt, const void *theta1, const void *theta2, const vo
   }
   S2V_LAUNCH_CHECK();
   return S2V_OK;
+}
+
+int s2v_embed_round_peers(s2v_dtype dt, const s2v_shard *sh, const void *theta4,
+                          const void *table, int K, int max_deg, const void *h_in, void *h_out,
+                          void *const *peer_outs, int npeers, void *m_out, void *stream) {
+  if (dt != S2V_F32 || K != 64)
+    return fail(S2V_EINVAL, "fused peer rounds need K = 64 fp32");
+  return embed_round_t<float>(sh, theta4, table, K, max_deg, h_in, h_out, m_out,
+                              as_stream(stream), (float *const *)peer_outs, npeers);
 }
 
 int s2v_embed_round(s2v_dtype dt, const s2v_shard *sh, const void *theta4, const void *table,

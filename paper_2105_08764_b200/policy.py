@@ -222,13 +222,25 @@ def _buffers(state: PartitionedState, k: int, dtype, count: int):
     return state.workspace(f"h{count}", (k, np.dtype(dtype).str, count), make)
 
 
-def _allgather_rows(state: PartitionedState, comm, h: torch.Tensor, k: int, tag: str):
-    """In-place halo all-gather of every slot's rank chunk (NCCL)."""
+def _peer_list(state: PartitionedState, dc, name: str, t: torch.Tensor, as_array: bool):
+    """Peer addresses of a workspace buffer, registered once per workspace
+    (a collective on every rank at the same point)."""
+    if not getattr(dc, "supports_push", False):
+        return None
+    key = (t.data_ptr(), t.numel(), as_array)
+    return state.workspace(f"peers:{name}", key,
+                           lambda: dc.peer_array(t) if as_array else dc.peers_of(t))
+
+
+def _allgather_rows(state: PartitionedState, comm, h: torch.Tensor, k: int, tag: str,
+                    name: str = ""):
+    """In-place halo all-gather of every slot's rank chunk (device transport)."""
     if state.world == 1:
         return
     dc = comm.device_comm()
     chunk = state.rows_max * k * h.element_size()
-    dc.allgather_slots(h.data_ptr(), chunk, chunk * state.world, state.batch, stream_ptr())
+    peers = _peer_list(state, dc, name or tag, h, False)
+    dc.allgather_rows(h, chunk, chunk * state.world, state.batch, stream_ptr(), peers=peers)
     comm.record(tag, state.rows_max * k * state.batch)
 
 
@@ -268,12 +280,24 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
             ev0.record()
-        _lib.call("s2v_embed_round", dt, state.shard_ref(), dparams.ptr("theta4"), ptr(table),
-                  k, max_deg, ptr(h_prev), ptr(h_out), ptr(m_out), st)
+        dc = comm.device_comm() if state.world > 1 else None
+        if dc is not None and dc.supports_push and k == 64 and dt == _lib.S2V_F32:
+            # fused halo exchange: the kernel stores each row into every peer
+            peers = _peer_list(state, dc, f"h{layer if tape else layer % 2}/{len(hs)}", h_out,
+                               True)
+            _lib.call("s2v_embed_round_peers", dt, state.shard_ref(), dparams.ptr("theta4"),
+                      ptr(table), k, max_deg, ptr(h_prev), ptr(h_out), ptr(peers), state.world,
+                      ptr(m_out), st)
+            dc.signal_and_wait(st)
+            comm.record("embed_fwd", state.rows_max * k * state.batch)
+        else:
+            _lib.call("s2v_embed_round", dt, state.shard_ref(), dparams.ptr("theta4"),
+                      ptr(table), k, max_deg, ptr(h_prev), ptr(h_out), ptr(m_out), st)
+            _allgather_rows(state, comm, h_out, k, "embed_fwd",
+                            name=f"h{layer if tape else layer % 2}/{len(hs)}")
         if timer is not None:
             ev1.record()
             timer.append((ev0, ev1))
-        _allgather_rows(state, comm, h_out, k, "embed_fwd")
         h_prev = h_out
         out.append(h_out)
     return out, ms, table
@@ -484,7 +508,7 @@ def loss_and_gradients(state: PartitionedState, actions, targets, params: Policy
                   None if last else ptr(ws["dm"]), s)
         if last:
             break
-        _allgather_rows(state, comm, ws["dm"], k, "embed_bwd")
+        _allgather_rows(state, comm, ws["dm"], k, "embed_bwd", name="dm")
         _lib.call("s2v_gather", dt, state.shard_ref(), k, ptr(ws["dm"]), ptr(ws["grad_h"]), s)
     _lib.call("s2v_param_grads", dt, state.shard_ref(), k, dparams.ptr("theta2"),
               dparams.ptr("theta3"), ptr(ws["dzsum"]), ptr(ws["pp"]), s)
