@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
   __shared__ __align__(16) float thT[64][64 + 4];        // thT[p][k] = theta4[k][p]
   __shared__ __align__(16) float ms[kTileRows][64 + 4];  // m tile
   __shared__ int32_t s_rows[kTileRows];
+  __shared__ int64_t s_e0[kTileRows], s_e1[kTileRows];  // neighbour range, empty if in S
   __shared__ int s_tile;
   for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x)
     thT[idx % 64][idx / 64] = theta4[idx];
@@ -153,8 +154,17 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
     if (tid < kTileRows) {
+      // one pass loads every row's id, range and membership in S
       const int64_t q = first + tile * kTileRows + tid;
-      s_rows[tid] = q < nrows ? (sh.order ? sh.order[q] : (int32_t)q) : -1;
+      const int32_t r = q < nrows ? (sh.order ? sh.order[q] : (int32_t)q) : -1;
+      s_rows[tid] = r;
+      int64_t e0 = 0, e1 = 0;
+      if (r >= 0 && h_in && !sh.sol[r]) {
+        e0 = sh.row_ptr[r];
+        e1 = sh.row_ptr[r + 1];
+      }
+      s_e0[tid] = e0;
+      s_e1[tid] = e1;
     }
     __syncthreads();
     // ---- gather: each half-warp handles rows hw and hw+16 of the tile
@@ -163,9 +173,9 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       const int lr = hw + 16 * q;
       const int64_t r = s_rows[lr];
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (h_in && r >= 0 && !sh.sol[r])
-        acc = gather_row64(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, h_in, sub, hmask, hbase,
-                           hot_rows, pol_hot, pol_cold);
+      if (s_e1[lr] > s_e0[lr])
+        acc = gather_row64(s_e0[lr], s_e1[lr], sh.cols, h_in, sub, hmask, hbase, hot_rows,
+                           pol_hot, pol_cold);
       *reinterpret_cast<float4 *>(&ms[lr][sub * 4]) = acc;
       if (m_out && r >= 0) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
     }
