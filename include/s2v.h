@@ -152,6 +152,25 @@ int s2v_score_blocks(const s2v_shard *sh);
 int s2v_topk_merge(const s2v_shard *sh, const uint64_t *block_keys, int d, uint64_t *top,
                    void *stream);
 
+/* ---- device-resident selection loop ----------------------- */
+/* u1 = g @ theta5.T in numpy/OpenBLAS order (policy.py:201): B == 1 sgemv
+ * order (K % 8 == 0, K >= 16) or B >= 32 sequential FMA; s2v_u1_exact tells
+ * whether a (B, K) pair is covered (else the host computes u1 with numpy). */
+int s2v_u1(s2v_dtype dt, int B, int K, const void *g, const void *theta5, void *u1,
+           void *stream);
+int s2v_u1_exact(int B, int K);
+/* d = SelectionSchedule.d_for(count, N) and the first d keys as picks for
+ * every active slot (inference.py:54-73,116-124); error = 1 on an active slot
+ * without candidates ("empty candidate set"). */
+int s2v_select(int B, int dmax, int64_t N, const double *fracs, const int *ds, int nthr,
+               int fallback, const int64_t *counts, const uint64_t *keys, const uint8_t *active,
+               int64_t *picks, int32_t *evaluated, int32_t *error, void *stream);
+/* Append one evaluation (picks, applied, evaluated) to the trace and set
+ * active = residual > 0 (inference.py:147). */
+int s2v_trace(int B, int dmax, const int64_t *picks, const uint8_t *applied,
+              const int32_t *evaluated, const int64_t *residual, uint8_t *active,
+              int64_t *trace_picks, uint8_t *trace_applied, int32_t *trace_eval, void *stream);
+
 /* ---- policy backward + Adam (policy.py:232-359) -------------------------- */
 /* Number of CTAs (= partial rows) used by the backward reductions. */
 int s2v_backward_blocks(const s2v_shard *sh);

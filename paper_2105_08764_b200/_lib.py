@@ -68,6 +68,10 @@ _SIGNATURES = {
     "s2v_score": ([_I, _SH, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P], _I),
     "s2v_score_blocks": ([_SH], _I),
     "s2v_topk_merge": ([_SH, _P, _I, _P, _P], _I),
+    "s2v_u1": ([_I, _I, _I, _P, _P, _P, _P], _I),
+    "s2v_u1_exact": ([_I, _I], _I),
+    "s2v_select": ([_I, _I, _I64, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P], _I),
+    "s2v_trace": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     "s2v_backward_blocks": ([_SH], _I),
     "s2v_grad_h_init": ([_I, _SH, _I, _P, _P, _P, _P, _P], _I),
     "s2v_layer_backward": ([_I, _SH, _I, _P, _P, _P, _P, _P, _P, _I, _P, _P], _I),
@@ -143,6 +147,7 @@ KERNELS_PER_CALL = {
     "s2v_embed_round": 1, "s2v_embed_round_peers": 1, "s2v_colsum": 2, "s2v_score": 1, "s2v_topk_merge": 1,
     "s2v_grad_h_init": 1, "s2v_layer_backward": 1, "s2v_gather": 1, "s2v_param_grads": 1,
     "s2v_reduce_partials": 1, "s2v_head_backward": 1, "s2v_adam": 1,
+    "s2v_u1": 1, "s2v_select": 1, "s2v_trace": 1,
 }
 launch_count = 0
 

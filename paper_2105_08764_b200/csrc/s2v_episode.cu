@@ -1,0 +1,148 @@
+// Device-resident selection loop pieces: the exact u1
+// product, the adaptive d rule with top-d picks, and the per-evaluation
+// trace -- so a whole policy evaluation + group apply runs without a host
+// round trip and can be captured in a CUDA graph.
+//
+// Replaces (paths relative to /root/reference):
+//   u1 = g @ theta5.T                      pkg/src/graphrl/policy.py:201
+//   SelectionSchedule.d_for / select_top_d pkg/src/graphrl/inference.py:54-73,116-124
+//   active = residual_counts > 0           pkg/src/graphrl/inference.py:147
+#include "s2v_common.cuh"
+
+namespace s2v {
+
+// u1[b][k] = sum_p theta5[k][p] g[b][p] in numpy/OpenBLAS (SkylakeX) order:
+//  B == 1 : sgemv -- two 4-lane FMA accumulators over p blocks of 4
+//           (block parity selects the accumulator), then (a0 + a1) per lane
+//           and ((l0 + l1) + (l2 + l3));  K % 8 == 0, K >= 16
+//  B >= 32: sgemm -- one sequential FMA chain per output
+// (identified against numpy 2.3 / OpenBLAS 0.3.30; pinned by the GPU tests,
+// whose oracle computes u1 with numpy itself).
+__global__ void u1_kernel(int B, int K, const float *__restrict__ g,
+                          const float *__restrict__ t5, float *__restrict__ u1) {
+  const int b = blockIdx.x;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const float *gb = g + (int64_t)b * K;
+    const float *row = t5 + (int64_t)k * K;
+    float out;
+    if (B == 1) {
+      float a[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      for (int p = 0; p < K; p++) {
+        const int u = (p >> 2) & 1, l = p & 3;
+        a[u][l] = __fmaf_rn(row[p], gb[p], a[u][l]);
+      }
+      float v[4];
+      for (int l = 0; l < 4; l++) v[l] = __fadd_rn(a[0][l], a[1][l]);
+      out = __fadd_rn(__fadd_rn(v[0], v[1]), __fadd_rn(v[2], v[3]));
+    } else {
+      float acc = 0.f;
+      for (int p = 0; p < K; p++) acc = __fmaf_rn(row[p], gb[p], acc);
+      out = acc;
+    }
+    u1[(int64_t)b * K + k] = out;
+  }
+}
+
+// Adaptive d and picks per slot (inference.py:116-124): d = first schedule
+// entry with count > frac * N (fp64 product, as Python), else fallback;
+// d = min(d, count); picks = the first d keys (descending score, lowest id on
+// ties).  keys: [B][dmax][2] {orderable score, ~node}; out: picks [B][dmax].
+struct Schedule {
+  double frac[8];
+  int d[8];
+  int n;
+  int fallback;
+};
+
+__global__ void select_kernel(int B, int dmax, int64_t N, Schedule sched,
+                              const int64_t *__restrict__ counts,
+                              const uint64_t *__restrict__ keys, const uint8_t *__restrict__ active,
+                              int64_t *__restrict__ picks, int32_t *__restrict__ evaluated,
+                              int32_t *__restrict__ error) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+    int d = 0;
+    if (active[b]) {
+      const int64_t c = counts[b];
+      if (c == 0) {
+        *error = 1;  // InvalidActionError("empty candidate set")
+      } else {
+        d = sched.fallback;
+        for (int i = 0; i < sched.n; i++)
+          if ((double)c > sched.frac[i] * (double)N) {
+            d = sched.d[i];
+            break;
+          }
+        if ((int64_t)d > c) d = (int)c;
+      }
+    }
+    evaluated[b] = active[b] ? 1 : 0;
+    for (int j = 0; j < dmax; j++)
+      picks[(int64_t)b * dmax + j] =
+          j < d ? (int64_t)(~keys[((int64_t)b * dmax + j) * 2 + 1]) : (int64_t)-1;
+  }
+}
+
+// After the group apply: append this evaluation to the trace and refresh
+// active = residual > 0 (P = 1: local residual is global).
+__global__ void trace_kernel(int B, int dmax, const int64_t *__restrict__ picks,
+                             const uint8_t *__restrict__ applied,
+                             const int32_t *__restrict__ evaluated,
+                             const int64_t *__restrict__ residual, uint8_t *__restrict__ active,
+                             int64_t *__restrict__ trace_picks, uint8_t *__restrict__ trace_applied,
+                             int32_t *__restrict__ trace_eval) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+    for (int j = 0; j < dmax; j++) {
+      trace_picks[(int64_t)b * dmax + j] = picks[(int64_t)b * dmax + j];
+      trace_applied[(int64_t)b * dmax + j] = applied[(int64_t)b * dmax + j];
+    }
+    trace_eval[b] = evaluated[b];
+    active[b] = residual[b] > 0 ? 1 : 0;
+  }
+}
+
+}  // namespace s2v
+
+using namespace s2v;
+
+extern "C" {
+
+int s2v_u1(s2v_dtype dt, int B, int K, const void *g, const void *theta5, void *u1,
+           void *stream) {
+  if (dt != S2V_F32) return fail(S2V_EINVAL, "device u1 is fp32 only");
+  if (!((B == 1 && K % 8 == 0 && K >= 16) || B >= 32))
+    return fail(S2V_EINVAL, "no exact device order for u1 with B=%d K=%d", B, K);
+  u1_kernel<<<B, 64, 0, as_stream(stream)>>>(B, K, (const float *)g, (const float *)theta5,
+                                             (float *)u1);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_u1_exact(int B, int K) { return (B == 1 && K % 8 == 0 && K >= 16) || B >= 32; }
+
+int s2v_select(int B, int dmax, int64_t N, const double *fracs, const int *ds, int nthr,
+               int fallback, const int64_t *counts, const uint64_t *keys, const uint8_t *active,
+               int64_t *picks, int32_t *evaluated, int32_t *error, void *stream) {
+  if (nthr > 8) return fail(S2V_EINVAL, "at most 8 schedule thresholds");
+  Schedule sc;
+  sc.n = nthr;
+  sc.fallback = fallback;
+  for (int i = 0; i < nthr; i++) {
+    sc.frac[i] = fracs[i];
+    sc.d[i] = ds[i];
+  }
+  select_kernel<<<1, 128, 0, as_stream(stream)>>>(B, dmax, N, sc, counts, keys, active, picks,
+                                                  evaluated, error);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_trace(int B, int dmax, const int64_t *picks, const uint8_t *applied,
+              const int32_t *evaluated, const int64_t *residual, uint8_t *active,
+              int64_t *trace_picks, uint8_t *trace_applied, int32_t *trace_eval, void *stream) {
+  trace_kernel<<<1, 128, 0, as_stream(stream)>>>(B, dmax, picks, applied, evaluated, residual,
+                                                 active, trace_picks, trace_applied, trace_eval);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+}  // extern "C"

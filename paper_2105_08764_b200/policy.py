@@ -319,8 +319,9 @@ def _as_device_embedding(embed, state_hint, params: PolicyParams, comm) -> Devic
     raise TypeError("q_forward needs the DeviceEmbedding returned by embed_forward")
 
 
-def _global_sum(emb: DeviceEmbedding) -> np.ndarray:
-    """g = pairwise sum over all N nodes of every slot (policy.py:199-200)."""
+def _colsum_device(emb: DeviceEmbedding) -> torch.Tensor:
+    """g = pairwise sum over all N nodes of every slot (policy.py:199-200),
+    left on the device ([B][K])."""
     st = emb.state
     k = emb.k
     wsb = _lib.load().s2v_colsum_workspace(st.shard_ref(), k, emb.dtype.itemsize)
@@ -330,18 +331,29 @@ def _global_sum(emb: DeviceEmbedding) -> np.ndarray:
         "g": torch.empty(st.batch * k, dtype=_torch_dtype(emb.dtype), device=st.device)})
     _lib.call("s2v_colsum", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h), ptr(ws["g"]),
               ptr(ws["ws"]), wsb, stream_ptr())
-    return ws["g"].to("cpu").numpy().reshape(st.batch, k)
+    return ws["g"]
+
+
+def _global_sum(emb: DeviceEmbedding) -> np.ndarray:
+    return _colsum_device(emb).to("cpu").numpy().reshape(emb.state.batch, emb.k)
+
+
+def u1_on_device(batch: int, k: int, dtype) -> bool:
+    """Whether libs2v reproduces numpy's g @ theta5.T order for this shape."""
+    return np.dtype(dtype) == np.float32 and bool(_lib.load().s2v_u1_exact(batch, k))
 
 
 def _score(emb: DeviceEmbedding, params: PolicyParams, dparams: _DeviceParams,
-           cand_override: np.ndarray | None, mode: int, d: int):
+           cand_override: np.ndarray | None, mode: int, d: int, readback: bool = True):
     """Run the scorer; returns (scores device tensor, top keys (B,d,2) or None,
     counts (B,))."""
     st = emb.state
     k = emb.k
-    g = _global_sum(emb)
-    # policy.py:201 -- the reference's own numpy product, on the host
-    u1 = np.ascontiguousarray(g @ params.theta5.T, dtype=params.dtype)
+    device_u1 = u1_on_device(st.batch, k, emb.dtype)
+    if not device_u1:
+        g = _global_sum(emb)
+        # policy.py:201 -- the reference's own numpy product, on the host
+        u1 = np.ascontiguousarray(g @ params.theta5.T, dtype=params.dtype)
     nblk = _lib.load().s2v_score_blocks(st.shard_ref())
     rows = st.batch * st.part.num_rows
     ws = st.workspace("score", (k, emb.dtype.str), lambda: {
@@ -350,7 +362,11 @@ def _score(emb: DeviceEmbedding, params: PolicyParams, dparams: _DeviceParams,
         "bkeys": torch.empty(st.batch * nblk * 8 * 2, dtype=torch.int64, device=st.device),
         "out": torch.empty(st.batch * (1 + 8 * 2), dtype=torch.int64, device=st.device),
         "cand": torch.empty(max(rows, 1), dtype=torch.uint8, device=st.device)})
-    ws["u1"].copy_(torch.from_numpy(u1.reshape(-1)))
+    if device_u1:  # numpy's own accumulation order, reproduced on device
+        _lib.call("s2v_u1", _dt_code(emb.dtype), st.batch, k, ptr(_colsum_device(emb)),
+                  dparams.ptr("theta5"), ptr(ws["u1"]), stream_ptr())
+    else:
+        ws["u1"].copy_(torch.from_numpy(u1.reshape(-1)))
     cand_ptr = None
     if cand_override is not None:
         ws["cand"][:rows].copy_(torch.from_numpy(
@@ -364,6 +380,8 @@ def _score(emb: DeviceEmbedding, params: PolicyParams, dparams: _DeviceParams,
     if d > 0:
         _lib.call("s2v_topk_merge", st.shard_ref(), ptr(ws["bkeys"]), d,
                   ws["out"].data_ptr() + 8 * st.batch, s)
+    if not readback:
+        return ws
     out = ws["out"].to("cpu").numpy()  # counts and keys in one read-back
     counts = out[:st.batch].copy()
     if d > 0:
@@ -401,6 +419,15 @@ def decode_keys(top: np.ndarray):
     vals = bits.view(np.float64).copy()
     vals[s == np.uint64(0xFFFFFFFFFFFFFFFF)] = np.nan
     return node, vals, valid
+
+
+def evaluate_device(state: PartitionedState, params: PolicyParams, dparams, comm, d: int,
+                    mode: int = 0):
+    """evaluate() without any host round trip (P = 1, device u1): returns the
+    score workspace whose "out" holds counts [B] then top-d keys [B][d][2]."""
+    hs, _, _ = _forward_rounds(state, dparams, params.num_layers, comm, params.dtype, False)
+    emb = DeviceEmbedding(state, hs[-1], params.embed_dim, params.dtype, gathered=True)
+    return _score(emb, params, dparams, None, mode, d, readback=False)
 
 
 def merge_rank_keys(top: np.ndarray, counts: np.ndarray, comm, d: int):
