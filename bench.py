@@ -261,6 +261,17 @@ def cpu_train_sample(dataset, B_sample, B, tau):
 # ---------------------------------------------------------------------------
 
 
+def make_stepper(P, state, params, comm, sched):
+    """One inference step exactly as solve() runs it: the device-resident loop
+    (DeviceEpisode, one evaluation per read-back) at P = 1, else solve_step."""
+    from paper_2105_08764_b200.inference import DeviceEpisode, _device_loop_ok, solve_step
+    if _device_loop_ok(state, params, comm, sched):
+        ep = DeviceEpisode(state, params, comm, sched, 1, use_graph=False)
+        return (lambda: ep.run_chunk()), "device episode loop (inference.DeviceEpisode)"
+    active = np.array([True] * state.batch)
+    return (lambda: solve_step(state, params, comm, sched, active)), "inference.solve_step"
+
+
 def infer_leg(P, comm, graph, steps, warmup, name):
     """Device time per inference step (solve_step) walking an episode from
     S = {}; stops early if the episode ends."""
@@ -270,9 +281,9 @@ def infer_leg(P, comm, graph, steps, warmup, name):
     params = P.PolicyParams.initialize(64, 5, seed=0)
     sched = P.SelectionSchedule.adaptive()
     state = P.PartitionedState([graph], part)
-    active = np.array([True])
+    step, path = make_stepper(P, state, params, comm, sched)
     for _ in range(warmup):
-        solve_step(state, params, comm, sched, active)
+        step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -280,14 +291,14 @@ def infer_leg(P, comm, graph, steps, warmup, name):
     for _ in range(steps):
         if int(state.local_residual.sum()) == 0:
             break
-        solve_step(state, params, comm, sched, active)
+        step()
         done += 1
     e1.record()
     torch.cuda.synchronize()
     rp, _ = graph.csr_arrays()
     deg = np.diff(rp)
     return {"workload": name, "value": e0.elapsed_time(e1) / max(done, 1) / 1e3, "unit": "s",
-            "steps": done, "warmup": warmup, "nodes": graph.num_nodes,
+            "steps": done, "warmup": warmup, "nodes": graph.num_nodes, "path": path,
             "edges": graph.num_edges, "max_degree": int(deg.max()),
             "hub_rows": int(state.n_hub), "isolated_frac": float(np.mean(deg == 0))}
 
@@ -355,8 +366,9 @@ def main():
     torch.cuda.synchronize()
     t_state = time.time() - t0
 
+    step, step_path = make_stepper(P, state, params, comm, sched)
     for _ in range(args.warmup):
-        solve_step(state, params, comm, sched, active)
+        step()
     torch.cuda.synchronize()
     barrier()
     launches0 = _lib.launch_count
@@ -368,7 +380,7 @@ def main():
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
         for _ in range(args.steps):
-            solve_step(state, params, comm, sched, active)
+            step()
         ev1.record()
         torch.cuda.synchronize()
         barrier()
@@ -379,7 +391,7 @@ def main():
     # CUDA events on the launching stream over one more step
     policy.ROUND_TIMER = []
     alive_now = int(state.local_residual.sum())
-    solve_step(state, params, comm, sched, active)
+    step()
     torch.cuda.synchronize()
     rounds = policy.ROUND_TIMER
     policy.ROUND_TIMER = None
@@ -494,7 +506,7 @@ def main():
                 "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic", "config": workload(args),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": int(launches), "clocks": clocks.summary(),
+                "gpu_launches": int(launches), "clocks": clocks.summary(), "step_path": step_path,
                 "train_steps": train,
                 "other_inference": extra,
                 "setup": {"graph_gen_s": round(t_gen, 2), "state_build_s": round(t_state, 3),
