@@ -1,0 +1,85 @@
+"""Full-size parity at BASELINE cfg3/cfg4 sizes (BA(2M,16): 32M edges) against
+digests of the reference's own outputs (oracle/make_golden_full.py): the
+GPU embedding and score arrays hash to the reference's bytes, g/u1 match,
+the first adaptive groups match pick for pick, and the cfg4 training step
+matches within 1e-4."""
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2105_08764_b200 as P
+from reference_math import scale_error
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def ba2m():
+    g = P.generate_ba(2_000_000, 16, 0)
+    g.csr_arrays()
+    return g
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_cfg3_forward_and_first_steps_match_reference(ba2m):
+    path = GOLD / "full_cfg3_infer.json"
+    if not path.exists():
+        pytest.skip("full-size golden not generated")
+    gold = json.loads(path.read_text())
+    params = P.PolicyParams.initialize(64, 5, seed=0)
+
+    def worker(comm):
+        part = P.partition_rows(ba2m.num_nodes, 1)[0]
+        st = P.PartitionedState([ba2m], part)
+        emb = P.embed_forward(st, params, comm)
+        h = emb.local_rows()[0].to("cpu").numpy()
+        sc = P.q_forward(emb, st.cand, params, comm)[0]
+        from paper_2105_08764_b200.policy import _global_sum
+        g = _global_sum(emb)[0]
+        cand = st.cand[0].copy()
+        steps = []
+        sched = P.SelectionSchedule.adaptive()
+        for _ in range(len(gold["first_steps_picks"])):
+            picks, _ = P.inference.solve_step(st, params, comm, sched, np.array([True]))
+            steps.append([int(v) for v in picks[0] if v >= 0])
+        return h, sc, g, cand, steps
+    h, sc, g, cand, steps = P.run_workers(1, worker)[0]
+    assert _sha(cand) == gold["cand_sha256"]
+    assert np.array_equal(g, np.asarray(gold["g"], np.float32))
+    assert np.array_equal(h[0], np.asarray(gold["h_row0"], np.float32))
+    assert _sha(h) == gold["h_sha256"]
+    assert _sha(sc) == gold["scores_sha256"]
+    assert steps == gold["first_steps_picks"]
+
+
+def test_cfg4_training_step_matches_reference(ba2m):
+    path = GOLD / "full_cfg4_train.json"
+    if not path.exists():
+        pytest.skip("full-size golden not generated")
+    gold = json.loads(path.read_text())
+    params = P.PolicyParams.initialize(64, 5, seed=0)
+    n = ba2m.num_nodes
+    snaps = np.zeros((2, n), np.uint8)
+    snaps[1, gold["snap1"]] = 1
+    batch = [P.ExperienceTuple(0, P.pack_solution(snaps[i]), gold["actions"][i], 0.0)
+             for i in range(2)]
+
+    def worker(comm):
+        part = P.partition_rows(n, 1)[0]
+        state = P.tuples_to_graphs(batch, [ba2m], part)
+        targets = P.batch_targets(batch, [ba2m], params, comm, part, 0.9).astype(np.float32)
+        loss, grads = P.loss_and_gradients(state, np.array(gold["actions"]), targets, params,
+                                           comm)
+        return targets, loss, grads
+    targets, loss, grads = P.run_workers(1, worker)[0]
+    assert np.array_equal(targets, np.asarray(gold["targets"], np.float32))
+    assert abs(loss - gold["loss"]) <= 1e-4 * abs(gold["loss"])
+    for k in P.PARAM_NAMES:
+        assert scale_error(grads[k], np.asarray(gold["grads"][k])).max() < 1e-4, k
