@@ -103,7 +103,10 @@ int s2v_shard_init(const s2v_shard *sh, const uint8_t *sol_phys, void *stream);
 int s2v_apply_phase1(const s2v_shard *sh, const int64_t *picks, int d, int64_t *info,
                      int validate, int32_t *err_out, void *stream);
 int s2v_apply_phase2(const s2v_shard *sh, const int64_t *picks, int d, const int64_t *info,
-                     uint8_t *applied, int64_t *removed, void *stream);
+                     uint8_t *applied, int64_t *removed, int first_forced, void *stream);
+/* (first_forced = 1: pick 0 is applied unconditionally, the reference's
+ * rule for the first pick of a group; groups larger than 64 are applied as
+ * consecutive sub-groups of 64 with first_forced = 0 after the first.) */
 
 /* ---- policy forward (pkg/src/graphrl/policy.py:144-224) ------------------ */
 /* e12 table: table[(deg)][K] for deg in [0,max_deg] (sol=0) and row max_deg+1
@@ -151,6 +154,15 @@ int s2v_score_blocks(const s2v_shard *sh);
  * A key is two uint64 {orderable(score), ~node}; {0,0} = none. */
 int s2v_topk_merge(const s2v_shard *sh, const uint64_t *block_keys, int d, uint64_t *top,
                    void *stream);
+/* For d > 8 (SelectionSchedule.fixed(d) allows any d): per-block top-8 of the
+ * selection keys strictly below ceiling[b] (the last key already taken),
+ * re-using the score pass's per-row keys (s2v_score_keys). */
+int s2v_score_keys(const s2v_shard *sh, const void *scores_f32, const uint8_t *cand, int mode,
+                   uint64_t *keys_all, void *stream);
+int s2v_score_keys_f64(const s2v_shard *sh, const void *scores_f64, const uint8_t *cand,
+                       int mode, uint64_t *keys_all, void *stream);
+int s2v_topk_below(const s2v_shard *sh, const uint64_t *keys_all, const uint64_t *ceiling,
+                   uint64_t *block_keys, void *stream);
 
 /* ---- device-resident selection loop ----------------------- */
 /* u1 = g @ theta5.T in numpy/OpenBLAS order (policy.py:201): B == 1 sgemv

@@ -732,6 +732,40 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
   if (tid == 0 && s_count) atomicAdd((unsigned long long *)&counts[b], s_count);
 }
 
+// Per-row selection keys from the scores (mode 0: candidates with a finite
+// score; mode 1: every candidate), for the d > 8 path.
+template <class T>
+__global__ void score_keys_kernel(s2v_shard sh, const T *__restrict__ scores,
+                                  const uint8_t *__restrict__ cand, int mode,
+                                  Key *__restrict__ keys) {
+  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = r % sh.num_rows;
+    const double s = (double)scores[r];
+    const bool ok = cand[r] && (isfinite(s) || mode == 1);
+    keys[r] = ok ? make_key(s, sh.row_start + i) : null_key();
+  }
+}
+
+// Per-block top-8 among keys strictly below ceiling[b].
+__global__ void topk_below_kernel(s2v_shard sh, const Key *__restrict__ keys,
+                                  const Key *__restrict__ ceiling, Key *__restrict__ block_keys) {
+  __shared__ Key s_keys[256 * kTopK];
+  const int b = blockIdx.y;
+  const Key ceil = ceiling[b];
+  Key top[kTopK];
+#pragma unroll
+  for (int q = 0; q < kTopK; q++) top[q] = null_key();
+  const int64_t i0 = (int64_t)blockIdx.x * kScoreRowsPerBlock;
+  const int64_t i1 = min(i0 + kScoreRowsPerBlock, sh.num_rows);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const Key k = keys[(int64_t)b * sh.num_rows + i];
+    if (key_gt(ceil, k)) insert_top(top, k);
+  }
+  block_merge_top(top, s_keys, block_keys + ((int64_t)b * gridDim.x + blockIdx.x) * kTopK);
+}
+
 __global__ void topk_merge_kernel(const Key *__restrict__ block_keys, int nblk, int d,
                                   Key *__restrict__ top_out) {
   extern __shared__ unsigned char smem_raw[];
@@ -920,6 +954,37 @@ int s2v_score(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, const voi
                                   cand_override, mode, (double *)scores, (Key *)block_keys,
                                   counts);
   }
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_score_keys(const s2v_shard *sh, const void *scores, const uint8_t *cand, int mode,
+                   uint64_t *keys_all, void *stream) {
+  int64_t rows = (int64_t)sh->batch * sh->num_rows;
+  if (rows == 0) return S2V_OK;
+  int grid = (int)std::min<int64_t>((rows + 255) / 256, kNumSMs * 8);
+  score_keys_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(*sh, (const float *)scores, cand,
+                                                                mode, (Key *)keys_all);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_score_keys_f64(const s2v_shard *sh, const void *scores, const uint8_t *cand, int mode,
+                       uint64_t *keys_all, void *stream) {
+  int64_t rows = (int64_t)sh->batch * sh->num_rows;
+  if (rows == 0) return S2V_OK;
+  int grid = (int)std::min<int64_t>((rows + 255) / 256, kNumSMs * 8);
+  score_keys_kernel<double><<<grid, 256, 0, as_stream(stream)>>>(
+      *sh, (const double *)scores, cand, mode, (Key *)keys_all);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_topk_below(const s2v_shard *sh, const uint64_t *keys_all, const uint64_t *ceiling,
+                   uint64_t *block_keys, void *stream) {
+  dim3 grid(s2v_score_blocks(sh), sh->batch);
+  topk_below_kernel<<<grid, 256, 0, as_stream(stream)>>>(*sh, (const Key *)keys_all,
+                                                         (const Key *)ceiling, (Key *)block_keys);
   S2V_LAUNCH_CHECK();
   return S2V_OK;
 }

@@ -126,7 +126,7 @@ __global__ void apply_phase1_kernel(s2v_shard sh, PartitionMap pm, const int64_t
 // earlier accepted picks it shares an alive edge with is > 0.  Returns the
 // accepted mask and the global number of removed entries (2 * rdeg at apply).
 __device__ uint64_t replay_group(const int64_t *picks, int d, const int64_t *info, int b,
-                                 long long *removed_global) {
+                                 long long *removed_global, int first_forced) {
   uint64_t amask = 0;
   long long rem = 0;
   for (int j = 0; j < d && j < 64; j++) {
@@ -135,7 +135,7 @@ __device__ uint64_t replay_group(const int64_t *picks, int d, const int64_t *inf
     int64_t deg = info[2 * ((int64_t)b * d + j)];
     const uint64_t adj = (uint64_t)info[2 * ((int64_t)b * d + j) + 1];
     if (j > 0) deg -= __popcll(adj & amask);
-    if (j == 0 || deg > 0) {
+    if ((j == 0 && first_forced) || deg > 0) {
       amask |= 1ull << j;
       rem += 2 * deg;
     }
@@ -149,13 +149,14 @@ __device__ uint64_t replay_group(const int64_t *picks, int d, const int64_t *inf
 // an edge between two accepted picks is counted exactly once; rdeg is
 // decremented atomically.  grid = (chunks, B).
 __global__ void apply_phase2_kernel(s2v_shard sh, const int64_t *picks, int d,
-                                    const int64_t *info, uint8_t *applied, int64_t *removed) {
+                                    const int64_t *info, uint8_t *applied, int64_t *removed,
+                                    int first_forced) {
   const int b = blockIdx.y;
   __shared__ uint64_t s_amask;
   __shared__ unsigned long long s_local;
   if (threadIdx.x == 0) {
     long long rem = 0;
-    s_amask = replay_group(picks, d, info, b, &rem);
+    s_amask = replay_group(picks, d, info, b, &rem, first_forced);
     s_local = 0;
     if (blockIdx.x == 0) {
       removed[b] = rem;
@@ -259,10 +260,11 @@ int s2v_apply_phase1(const s2v_shard *sh, const int64_t *picks, int d, int64_t *
 }
 
 int s2v_apply_phase2(const s2v_shard *sh, const int64_t *picks, int d, const int64_t *info,
-                     uint8_t *applied, int64_t *removed, void *stream) {
+                     uint8_t *applied, int64_t *removed, int first_forced, void *stream) {
   if (d < 1 || d > 64) return fail(S2V_EINVAL, "group size d=%d outside [1, 64]", d);
   dim3 grid(16, sh->batch);
-  apply_phase2_kernel<<<grid, 256, 0, as_stream(stream)>>>(*sh, picks, d, info, applied, removed);
+  apply_phase2_kernel<<<grid, 256, 0, as_stream(stream)>>>(*sh, picks, d, info, applied, removed,
+                                                           first_forced);
   S2V_LAUNCH_CHECK();
   apply_phase3_kernel<<<grid, 256, 0, as_stream(stream)>>>(*sh, picks, d, applied);
   S2V_LAUNCH_CHECK();

@@ -378,15 +378,47 @@ def _score(emb: DeviceEmbedding, params: PolicyParams, dparams: _DeviceParams,
               ptr(ws["scores"]), ptr(ws["bkeys"]), ptr(ws["out"]), s)
     top = None
     if d > 0:
-        _lib.call("s2v_topk_merge", st.shard_ref(), ptr(ws["bkeys"]), d,
+        _lib.call("s2v_topk_merge", st.shard_ref(), ptr(ws["bkeys"]), min(d, _lib.TOPK_MAX),
                   ws["out"].data_ptr() + 8 * st.batch, s)
     if not readback:
         return ws
     out = ws["out"].to("cpu").numpy()  # counts and keys in one read-back
     counts = out[:st.batch].copy()
     if d > 0:
-        top = out[st.batch:st.batch + st.batch * d * 2].view(np.uint64).reshape(st.batch, d, 2)
+        dm = min(d, _lib.TOPK_MAX)
+        top = out[st.batch:st.batch + st.batch * dm * 2].view(np.uint64).reshape(st.batch, dm, 2)
+        if d > _lib.TOPK_MAX:
+            top = _more_keys(st, ws, cand_ptr, mode, top.copy(), d)
     return ws["scores"][:rows], top, counts
+
+
+def _more_keys(st: PartitionedState, ws, cand_ptr, mode: int, top: np.ndarray, d: int):
+    """Top-d for d > 8 (SelectionSchedule.fixed(d) allows any d): per-row keys
+    once, then repeated top-8 passes strictly below the last key taken."""
+    rows = st.batch * st.part.num_rows
+    kw = st.workspace("keys_all", rows, lambda: {
+        "keys": torch.empty(max(rows, 1) * 2, dtype=torch.int64, device=st.device),
+        "ceil": torch.empty(st.batch * 2, dtype=torch.int64, device=st.device),
+        "top": torch.empty(st.batch * 8 * 2, dtype=torch.int64, device=st.device)})
+    s = stream_ptr()
+    fn = "s2v_score_keys" if ws["scores"].dtype == torch.float32 else "s2v_score_keys_f64"
+    _lib.call(fn, st.shard_ref(), ptr(ws["scores"]), cand_ptr or ptr(st.cand_d), mode,
+              ptr(kw["keys"]), s)
+    parts = [top]
+    have = top.shape[1]
+    while have < d:
+        last = parts[-1][:, -1, :]
+        if not np.any(last[:, 0]):  # every slot exhausted
+            break
+        kw["ceil"].copy_(torch.from_numpy(np.ascontiguousarray(last).view(np.int64).reshape(-1)))
+        _lib.call("s2v_topk_below", st.shard_ref(), ptr(kw["keys"]), ptr(kw["ceil"]),
+                  ptr(ws["bkeys"]), s)
+        _lib.call("s2v_topk_merge", st.shard_ref(), ptr(ws["bkeys"]), 8, ptr(kw["top"]), s)
+        nxt = kw["top"].to("cpu").numpy().view(np.uint64).reshape(st.batch, 8, 2).copy()
+        nxt[last[:, 0] == 0] = 0  # a slot already exhausted stays empty
+        parts.append(nxt)
+        have += 8
+    return np.concatenate(parts, axis=1)[:, :d]
 
 
 def q_forward(embed, cand: np.ndarray, params: PolicyParams, comm) -> np.ndarray:

@@ -285,8 +285,19 @@ class PartitionedState:
     def apply_groups(self, picks: np.ndarray, comm=None):
         """Apply a group of picks per slot with the mid-group skip rule
         (inference.py:125-146).  picks: (B, d) int64, -1 padded.  Returns
-        (applied (B, d) bool, removed (B,) global entries removed)."""
+        (applied (B, d) bool, removed (B,) global entries removed).  Groups
+        wider than 64 run as consecutive sub-groups of 64; only the group's
+        first pick is applied unconditionally, as in the reference."""
         picks = np.ascontiguousarray(picks, dtype=np.int64)
+        B, d = picks.shape
+        if d > 64:
+            parts = [self._apply_chunk(np.ascontiguousarray(picks[:, c:c + 64]), comm, c == 0)
+                     for c in range(0, d, 64)]
+            return (np.concatenate([a for a, _ in parts], axis=1),
+                    np.sum([r for _, r in parts], axis=0))
+        return self._apply_chunk(picks, comm, True)
+
+    def _apply_chunk(self, picks: np.ndarray, comm, first_forced: bool):
         B, d = picks.shape
         ws = self.workspace("apply", d, lambda: {
             "picks": torch.empty(B * d, dtype=torch.int64, device=self.device),
@@ -297,7 +308,7 @@ class PartitionedState:
         st = stream_ptr()
         _lib.call("s2v_apply_phase1", self.shard_ref(), ptr(ws["picks"]), d, ptr(ws["info"]), 0,
                   None, st)
-        if self.world > 1 and d > 1:
+        if self.world > 1 and (d > 1 or not first_forced):
             dc = comm.device_comm() if comm is not None else None
             if dc is None:
                 raise InvalidActionError("a sharded state needs its comm to apply picks")
@@ -305,7 +316,7 @@ class PartitionedState:
         out = ws["out"]
         base = out.data_ptr()
         _lib.call("s2v_apply_phase2", self.shard_ref(), ptr(ws["picks"]), d, ptr(ws["info"]),
-                  base + 16 * B, base, st)
+                  base + 16 * B, base, 1 if first_forced else 0, st)
         _lib.call("s2v_memcpy_async", base + 8 * B, ptr(self.residual_d), 8 * B, st)
         self.invalidate()
         host = out.to("cpu").numpy()
