@@ -156,27 +156,37 @@ class PartitionedState:
         np.cumsum([s.nnz for s in structs], out=ent_off[1:])
         self.nnz = int(ent_off[-1])
         slot_stride = P * self.rows_max
-        # block-diagonal assembly over slots (device-to-device, structure cached)
-        rp = [s.row_ptr[:-1] + int(ent_off[b]) for b, s in enumerate(structs)]
-        rp.append(torch.tensor([self.nnz], dtype=torch.int64, device=dev))
-        self.row_ptr = torch.cat(rp)
-        self.cols = torch.cat([s.cols0 + int(b * slot_stride) if b else s.cols0.clone()
-                               for b, s in enumerate(structs)]) if self.nnz else \
-            torch.zeros(1, dtype=torch.int32, device=dev)
-        cp = [s.col_ptr[:-1] + int(ent_off[b]) for b, s in enumerate(structs)]
-        cp.append(torch.tensor([self.nnz], dtype=torch.int64, device=dev))
-        self.col_ptr = torch.cat(cp)
-        self.col_ent = torch.cat([s.col_ent + int(ent_off[b]) for b, s in enumerate(structs)]) \
-            if self.nnz else torch.zeros(1, dtype=torch.int64, device=dev)
-        self.col_row = torch.cat([s.col_row + int(b * rows) for b, s in enumerate(structs)]) \
-            if self.nnz else torch.zeros(1, dtype=torch.int32, device=dev)
-        # hub rows of every slot first, then the remaining rows of every slot
-        if rows:
-            self.order = torch.cat(
-                [s.order[:s.n_hub] + int(b * rows) for b, s in enumerate(structs)] +
-                [s.order[s.n_hub:] + int(b * rows) for b, s in enumerate(structs)])
+        if batch == 1 and self.nnz:
+            # one slot: the cached read-only structure is used in place; only
+            # the column array (which carries the removed-edge bits) is copied
+            s0 = structs[0]
+            self.row_ptr, self.col_ptr, self.col_ent, self.col_row = (
+                s0.row_ptr, s0.col_ptr, s0.col_ent, s0.col_row)
+            self.cols = s0.cols0.clone()
+            self.order = s0.order if rows else torch.zeros(1, dtype=torch.int32, device=dev)
         else:
-            self.order = torch.zeros(1, dtype=torch.int32, device=dev)
+            # block-diagonal assembly over slots (device-to-device, structure cached)
+            rp = [s.row_ptr[:-1] + int(ent_off[b]) for b, s in enumerate(structs)]
+            rp.append(torch.tensor([self.nnz], dtype=torch.int64, device=dev))
+            self.row_ptr = torch.cat(rp)
+            self.cols = torch.cat([s.cols0 + int(b * slot_stride) if b else s.cols0.clone()
+                                   for b, s in enumerate(structs)]) if self.nnz else \
+                torch.zeros(1, dtype=torch.int32, device=dev)
+            cp = [s.col_ptr[:-1] + int(ent_off[b]) for b, s in enumerate(structs)]
+            cp.append(torch.tensor([self.nnz], dtype=torch.int64, device=dev))
+            self.col_ptr = torch.cat(cp)
+            self.col_ent = torch.cat([s.col_ent + int(ent_off[b])
+                                      for b, s in enumerate(structs)]) \
+                if self.nnz else torch.zeros(1, dtype=torch.int64, device=dev)
+            self.col_row = torch.cat([s.col_row + int(b * rows) for b, s in enumerate(structs)]) \
+                if self.nnz else torch.zeros(1, dtype=torch.int32, device=dev)
+            # hub rows of every slot first, then the remaining rows of every slot
+            if rows:
+                self.order = torch.cat(
+                    [s.order[:s.n_hub] + int(b * rows) for b, s in enumerate(structs)] +
+                    [s.order[s.n_hub:] + int(b * rows) for b, s in enumerate(structs)])
+            else:
+                self.order = torch.zeros(1, dtype=torch.int32, device=dev)
         self.n_hub = sum(s.n_hub for s in structs)
         nr = max(batch * rows, 1)
         self.rdeg = torch.zeros(nr, dtype=torch.int32, device=dev)
