@@ -14,6 +14,8 @@
 // fixed-order fp64 reduction over CTAs: deterministic, hence bit-identical
 // replicas on every rank.  Adam follows the reference's element-wise fp32
 // rounding sequence exactly.
+#include <cstdlib>
+
 #include "s2v_common.cuh"
 #include "s2v_gather.cuh"
 
@@ -350,32 +352,34 @@ __global__ void __launch_bounds__(256, 2) layer_backward64_kernel(
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * kT64;
     __syncthreads();
-    for (int e = tid; e < kT64 * 16; e += 256) {
-      const int row = e >> 4, c4 = e & 15;
+    float4 G[kT64 / 16], H[kT64 / 16], O[kT64 / 16], M[kT64 / 16];
+#pragma unroll
+    for (int q = 0; q < kT64 / 16; q++) {  // every load in flight before any use
+      const int e = tid + q * 256, row = e >> 4, c4 = e & 15;
       const int64_t r = r0 + row;
-      float4 dz = make_float4(0.f, 0.f, 0.f, 0.f), mv = dz;
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      G[q] = H[q] = O[q] = M[q] = z4;
       if (r < nrows) {
-        const float4 g = f4(grad_h + r * 64 + 4 * c4);
-        const float4 hv = f4(h_l + phys_of_row(sh, r) * 64 + 4 * c4);
-        dz.x = hv.x > 0.f ? g.x : 0.f;
-        dz.y = hv.y > 0.f ? g.y : 0.f;
-        dz.z = hv.z > 0.f ? g.z : 0.f;
-        dz.w = hv.w > 0.f ? g.w : 0.f;
-        float *ds = dzsum + r * 64 + 4 * c4;
-        if (first) {
-          st4(ds, dz);
-        } else {
-          float4 o = f4(ds);
-          o.x += dz.x;
-          o.y += dz.y;
-          o.z += dz.z;
-          o.w += dz.w;
-          st4(ds, o);
-        }
-        if (m_l) mv = f4(m_l + r * 64 + 4 * c4);
+        G[q] = f4(grad_h + r * 64 + 4 * c4);
+        H[q] = f4(h_l + phys_of_row(sh, r) * 64 + 4 * c4);
+        if (!first) O[q] = f4(dzsum + r * 64 + 4 * c4);
+        if (m_l) M[q] = f4(m_l + r * 64 + 4 * c4);
       }
+    }
+#pragma unroll
+    for (int q = 0; q < kT64 / 16; q++) {
+      const int e = tid + q * 256, row = e >> 4, c4 = e & 15;
+      const int64_t r = r0 + row;
+      float4 dz;
+      dz.x = H[q].x > 0.f ? G[q].x : 0.f;
+      dz.y = H[q].y > 0.f ? G[q].y : 0.f;
+      dz.z = H[q].z > 0.f ? G[q].z : 0.f;
+      dz.w = H[q].w > 0.f ? G[q].w : 0.f;
+      if (r < nrows)
+        st4(dzsum + r * 64 + 4 * c4, make_float4(O[q].x + dz.x, O[q].y + dz.y, O[q].z + dz.z,
+                                                 O[q].w + dz.w));
       st4(&dzs[row][4 * c4], dz);
-      st4(&ms[row][4 * c4], mv);
+      st4(&ms[row][4 * c4], M[q]);
     }
     __syncthreads();
     if (m_l) {
@@ -422,6 +426,215 @@ __global__ void __launch_bounds__(256, 2) layer_backward64_kernel(
 #pragma unroll
     for (int c = 0; c < 4; c++)
       partial[(int64_t)blockIdx.x * 4096 + (4 * lo + a) * 64 + 4 * hi + c] = p4[a][c];
+}
+
+// ---------------------------------------------------------------------------
+// Layer backward with dm = dz theta4 on the 5th-generation tensor cores.
+//
+// dm is GEMM-shaped (M = 128 rows, N = 64, K = 64) and its parity bar is
+// 1e-4, not bitwise, so it runs as tcgen05.mma kind::tf32 with 3xTF32 error
+// compensation (dz = hi + lo, theta4 = hi + lo; hi*hi + hi*lo + lo*hi,
+// fp32 accumulation in TMEM): ~2^-21 relative per product, fp32-class.
+// Operands are staged K-major in shared memory in the canonical
+// SWIZZLE_NONE core-matrix layout [k/4][row/8][8][4]; one thread issues the
+// 24 MMAs of a tile, tcgen05.commit signals an mbarrier, and warps 0-3 read
+// the 128 x 64 fp32 accumulator back with tcgen05.ld (one row per thread).
+// The dtheta4 reduction (64 x 64 over the tile rows) runs on the FFMA pipes
+// meanwhile.
+// ---------------------------------------------------------------------------
+constexpr int kTC = 128;  // rows per tile = MMA M
+
+__device__ __forceinline__ float tf32_hi(float v) {
+  return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); layout SWIZZLE_NONE
+  return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) layer_backward64_tc_kernel(
+    s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ grad_h,
+    const float *__restrict__ h_l, const float *__restrict__ m_l, float *__restrict__ dzsum,
+    float *__restrict__ partial, int first, float *__restrict__ dm_out) {
+  extern __shared__ __align__(1024) float tc_smem[];
+  float *a_hi = tc_smem;               // [16][16][8][4]
+  float *a_lo = a_hi + kTC * 64;
+  float *b_hi = a_lo + kTC * 64;       // [16][8][8][4]
+  float *b_lo = b_hi + 64 * 64;
+  float(*dzs)[68] = reinterpret_cast<float(*)[68]>(b_lo + 64 * 64);
+  float(*ms)[68] = reinterpret_cast<float(*)[68]>(b_lo + 64 * 64 + kTC * 68);
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // B = theta4^T (n = j, k), K-major, split hi / lo
+  for (int idx = tid; idx < 64 * 64; idx += 256) {
+    const int j = idx >> 6, k = idx & 63;
+    const float v = theta4[k * 64 + j];
+    const float hi = tf32_hi(v);
+    const int off = (((k >> 2) * 8 + (j >> 3)) * 8 + (j & 7)) * 4 + (k & 3);
+    b_hi[off] = hi;
+    b_lo[off] = v - hi;
+  }
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&mbar);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_slot;
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (8u << 17) | (8u << 24);
+  const uint32_t sa_hi = (uint32_t)__cvta_generic_to_shared(a_hi);
+  const uint32_t sa_lo = (uint32_t)__cvta_generic_to_shared(a_lo);
+  const uint32_t sb_hi = (uint32_t)__cvta_generic_to_shared(b_hi);
+  const uint32_t sb_lo = (uint32_t)__cvta_generic_to_shared(b_lo);
+  const int lo = tid & 15, hi = tid >> 4;
+  float p4[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+      p4[a][c] = first ? 0.f : partial[(int64_t)blockIdx.x * 4096 + (4 * lo + a) * 64 + 4 * hi + c];
+  uint32_t phase = 0;
+  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  const int64_t ntiles = (nrows + kTC - 1) / kTC;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kTC;
+    __syncthreads();
+    // all of this thread's loads first (8 x 4 float4 in flight), then compute
+    float4 G[kTC / 16], H[kTC / 16], O[kTC / 16], M[kTC / 16];
+#pragma unroll
+    for (int q = 0; q < kTC / 16; q++) {
+      const int e = tid + q * 256, row = e >> 4, c4 = e & 15;
+      const int64_t r = r0 + row;
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      G[q] = H[q] = O[q] = M[q] = z4;
+      if (r < nrows) {
+        G[q] = f4(grad_h + r * 64 + 4 * c4);
+        H[q] = f4(h_l + phys_of_row(sh, r) * 64 + 4 * c4);
+        if (!first) O[q] = f4(dzsum + r * 64 + 4 * c4);
+        if (m_l) M[q] = f4(m_l + r * 64 + 4 * c4);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kTC / 16; q++) {
+      const int e = tid + q * 256, row = e >> 4, c4 = e & 15;
+      const int64_t r = r0 + row;
+      float4 dz;
+      dz.x = H[q].x > 0.f ? G[q].x : 0.f;
+      dz.y = H[q].y > 0.f ? G[q].y : 0.f;
+      dz.z = H[q].z > 0.f ? G[q].z : 0.f;
+      dz.w = H[q].w > 0.f ? G[q].w : 0.f;
+      if (r < nrows)
+        st4(dzsum + r * 64 + 4 * c4, make_float4(O[q].x + dz.x, O[q].y + dz.y, O[q].z + dz.z,
+                                                 O[q].w + dz.w));
+      st4(&dzs[row][4 * c4], dz);
+      st4(&ms[row][4 * c4], M[q]);
+      const int aoff = ((c4 * 16 + (row >> 3)) * 8 + (row & 7)) * 4;
+      const float4 h4 = make_float4(tf32_hi(dz.x), tf32_hi(dz.y), tf32_hi(dz.z), tf32_hi(dz.w));
+      st4(a_hi + aoff, h4);
+      st4(a_lo + aoff, make_float4(dz.x - h4.x, dz.y - h4.y, dz.z - h4.z, dz.w - h4.w));
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (dm_out && tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t as[3] = {sa_hi, sa_hi, sa_lo};
+      const uint32_t bs[3] = {sb_hi, sb_lo, sb_hi};
+#pragma unroll
+      for (int sk = 0; sk < 8; sk++)
+#pragma unroll
+        for (int q = 0; q < 3; q++)
+          mma_tf32(tmem, umma_desc_kmajor(as[q] + sk * 2 * 2048, 2048, 128),
+                   umma_desc_kmajor(bs[q] + sk * 2 * 1024, 1024, 128), idesc,
+                   (sk | q) ? 1u : 0u);
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
+                       "r"(bar)
+                   : "memory");
+    }
+    if (m_l) {
+#pragma unroll 4
+      for (int row = 0; row < kTC; row++) {
+        const float4 d = f4(&dzs[row][4 * lo]);
+        const float4 m = f4(&ms[row][4 * hi]);
+        const float dv[4] = {d.x, d.y, d.z, d.w}, mvv[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int c = 0; c < 4; c++) p4[a][c] = __fmaf_rn(dv[a], mvv[c], p4[a][c]);
+      }
+    }
+    if (dm_out) {
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (warp < 4) {
+        const int64_t r = r0 + 32 * warp + lane;
+#pragma unroll
+        for (int cb = 0; cb < 4; cb++) {
+          uint32_t v[16];
+          const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + 16 * cb;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+              "%10, %11, %12, %13, %14, %15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (r < nrows) {
+            float *dst = dm_out + phys_of_row(sh, r) * 64 + 16 * cb;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              st4(dst + 4 * q, make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                           __uint_as_float(v[4 * q + 2]),
+                                           __uint_as_float(v[4 * q + 3])));
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+      partial[(int64_t)blockIdx.x * 4096 + (4 * lo + a) * 64 + 4 * hi + c] = p4[a][c];
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
 }
 
 // dtheta1 [64], dtheta2 [64], dtheta3 [64][64] partials from dzsum.
@@ -615,6 +828,22 @@ template <class T>
 static int layer_backward_t(const s2v_shard *sh, int K, const void *theta4, const void *grad_h,
                             const void *h_l, const void *m_l, void *dzsum, void *partial,
                             int first, void *dm_out, cudaStream_t st) {
+  // tcgen05 3xTF32 dm path: parity-verified, opt-in (S2V_BWD_TC=1) because
+  // at 1 CTA/SM it measures slower than the FFMA kernel
+  static const bool use_tc = [] {
+    const char *e = getenv("S2V_BWD_TC");
+    return e && e[0] == '1';
+  }();
+  if (sizeof(T) == 4 && K == 64 && use_tc) {
+    const size_t smem = sizeof(float) * (2 * kTC * 64 + 2 * 64 * 64 + 2 * kTC * 68);
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(layer_backward64_tc_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    layer_backward64_tc_kernel<<<bwd_blocks(*sh), 256, smem, st>>>(
+        *sh, (const float *)theta4, (const float *)grad_h, (const float *)h_l,
+        (const float *)m_l, (float *)dzsum, (float *)partial, first, (float *)dm_out);
+    S2V_LAUNCH_CHECK();
+    return S2V_OK;
+  }
   if (sizeof(T) == 4 && K == 64) {
     const size_t smem = sizeof(float) * 3 * 64 * 68;
     S2V_CUDA_CHECK(cudaFuncSetAttribute(layer_backward64_kernel,

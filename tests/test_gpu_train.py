@@ -116,3 +116,19 @@ def test_loss_and_gradients_with_hub_rows_vs_port():
     assert abs(loss - loss_o) <= 1e-4 * max(1.0, abs(loss_o))
     for k in P.PARAM_NAMES:
         assert scale_error(grads[k], grads_o[k]).max() < 1e-4, k
+
+
+def test_tensor_core_backward_path_vs_port():
+    """The opt-in tcgen05 (3xTF32) dm kernel: same K=64 parity cases, run in a
+    child process because the path is chosen once per process (S2V_BWD_TC)."""
+    import os
+    import subprocess
+    import sys
+    here = Path(__file__).resolve().parent
+    env = dict(os.environ, S2V_BWD_TC="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        str(here / "test_gpu_train.py"), "-k",
+                        "(vs_port and 64) or hub or ba1000", "-m", "gpu"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
