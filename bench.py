@@ -411,7 +411,9 @@ def main():
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "traffic_source": "profiles/r1_round64_traffic.json (ncu dram__bytes_read+write)",
-                "kernel": "round64_kernel (fused gather-SpMM + theta4 FMA chain + e12 + relu)",
+                "kernel": "round64_kernel (fused gather-SpMM + theta4 FMA chain + e12 + relu), "
+                          "rounds 3..5 (round 2 gathers the per-degree h1 table, round 1 is "
+                          "skipped)",
                 "round_ms": round(round_ms, 4), "algorithmic_bytes_per_launch": algo_bytes,
                 "peak_source": peak_src,
                 "bytes_model": "8(rows+1) row_ptr + 4 nnz cols + 256 alive gathers + 256 rows h_out"

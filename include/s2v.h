@@ -131,6 +131,20 @@ int s2v_embed_round_peers(s2v_dtype dt, const s2v_shard *sh, const void *theta4,
                           const void *table, int K, int max_deg, const void *h_in, void *h_out,
                           void *const *peer_outs, int npeers, void *m_out, void *stream);
 
+/* Round-1 outputs per e12 row: h1_table[t][k] = relu(table[t][k] + theta4 . 0)
+ * with the round kernel's exact operation order, t in [0, max_deg+1].
+ * K = 64 fp32. */
+int s2v_h1_table(s2v_dtype dt, const void *theta4, const void *table, int K, int max_deg,
+                 void *h1_table, void *stream);
+/* Embedding round 2 at P = 1 without reading h1: round 1's output row of an
+ * alive neighbour u (never in S) is h1_table[rdeg[u]], so the gather reads
+ * the L1/L2-resident table instead of the 256-byte rows of h1.  Same result
+ * bits as s2v_embed_round(h_in = h1).  Replaces the second iteration of
+ * policy.py:163-174.  K = 64 fp32, world = 1. */
+int s2v_embed_round2_table(s2v_dtype dt, const s2v_shard *sh, const void *theta4,
+                           const void *table, int K, int max_deg, const void *h1_table,
+                           void *h_out, void *m_out, void *stream);
+
 /* g[b][k] = numpy pairwise sum over the N nodes of slot b of h[.,k]; h must
  * hold every rank's rows (after an all-gather when P>1).  Replaces
  * embed.sum(axis=2) + q_fwd all-reduce (policy.py:199-200). */

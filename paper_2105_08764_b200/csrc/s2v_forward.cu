@@ -125,8 +125,28 @@ __global__ void __launch_bounds__(256) round_generic_kernel(
 //           thread produces 2 rows x 4 k (float4 store), FMA chain p=0..63,
 //           then z = e12[deg] + chain, relu.
 // ---------------------------------------------------------------------------
+//  TABLE  : round 2 at P = 1 reads neighbour rows from the per-degree table
+//           of round-1 outputs (h1_table_kernel) instead of h1: h1[u] depends
+//           only on (sol[u], rdeg[u]) and an alive neighbour has sol = 0, so
+//           h1[u] == h1_table[rdeg[u]] bit for bit and the same ascending
+//           adds give the same sums; the 2.4 MB table stays in L1/L2, so the
+//           round reads the CSR and rdeg instead of 16 GB of neighbour rows.
 constexpr int kTileRows = 32;
 
+// h1_table[t][k] = the round-1 output of a row whose e12 row is t: the
+// round kernel's epilogue with m = 0 (FMA chain over zeros, + e12, relu).
+__global__ void h1_table_kernel(const float *__restrict__ theta4,
+                                const float *__restrict__ table, int rows,
+                                float *__restrict__ h1) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)rows * 64) return;
+  const int k = (int)(idx & 63);
+  float z = 0.f;
+  for (int p = 0; p < 64; p++) z = __fmaf_rn(theta4[k * 64 + p], 0.f, z);
+  h1[idx] = relu(__fadd_rn(table[idx], z));
+}
+
+template <bool TABLE>
 __global__ void __launch_bounds__(256, 4) round64_kernel(
     s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ table, int max_deg,
     const float *__restrict__ h_in, float *__restrict__ h_out, float *__restrict__ m_out,
@@ -174,8 +194,8 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       const int64_t r = s_rows[lr];
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       if (s_e1[lr] > s_e0[lr])
-        acc = gather_row64(s_e0[lr], s_e1[lr], sh.cols, h_in, sub, hmask, hbase, hot_rows,
-                           pol_hot, pol_cold);
+        acc = gather_row64<TABLE>(s_e0[lr], s_e1[lr], sh.cols, h_in, sub, hmask, hbase,
+                                  hot_rows, pol_hot, pol_cold, sh.rdeg);
       *reinterpret_cast<float4 *>(&ms[lr][sub * 4]) = acc;
       if (m_out && r >= 0) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
     }
@@ -225,6 +245,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
 // gather (hub_gather_row64), then the same e12 + theta4 chain + relu epilogue
 // computed by 64 threads.  Runs on a side stream concurrently with
 // round64_kernel, which handles every other row.
+template <bool TABLE>
 __global__ void __launch_bounds__(256, 1) hub_round64_kernel(
     s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ table, int max_deg,
     const float *__restrict__ h_in, float *__restrict__ h_out, float *__restrict__ m_out,
@@ -246,8 +267,8 @@ __global__ void __launch_bounds__(256, 1) hub_round64_kernel(
     const int64_t r = sh.order[q];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (h_in && !sh.sol[r])
-      acc = hub_gather_row64(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, h_in, ring, hot_rows,
-                             pol_hot, pol_cold);
+      acc = hub_gather_row64<TABLE>(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, h_in, ring,
+                                    hot_rows, pol_hot, pol_cold, sh.rdeg);
     if (tid < 16) {
       *reinterpret_cast<float4 *>(mrow + sub * 4) = acc;
       if (m_out) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
@@ -795,9 +816,12 @@ __global__ void topk_merge_kernel(const Key *__restrict__ block_keys, int nblk, 
 template <class T>
 static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *table, int K,
                          int max_deg, const void *h_in, void *h_out, void *m_out,
-                         cudaStream_t st, float *const *peers = nullptr, int npeers = 0) {
+                         cudaStream_t st, float *const *peers = nullptr, int npeers = 0,
+                         bool from_table = false) {
   const int64_t nrows = (int64_t)sh->batch * sh->num_rows;
   if (nrows == 0) return S2V_OK;
+  if (from_table && !(sizeof(T) == 4 && K == 64 && sh->world == 1 && !npeers))
+    return fail(S2V_EINVAL, "degree-table rounds need K = 64 fp32 at P = 1");
   if (sizeof(T) == 4 && K == 64) {
     static thread_local int *counter = nullptr;
     if (!counter) S2V_CUDA_CHECK(cudaMalloc(&counter, sizeof(int)));
@@ -814,19 +838,20 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
     }();
     hot_rows = (uint32_t)(((uint64_t)hot_env << 20) / 256);
     SideStream *ss = nullptr;
-    S2V_CUDA_CHECK(cudaFuncSetAttribute(hub_round64_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto hub_kern = from_table ? &hub_round64_kernel<true> : &hub_round64_kernel<false>;
+    auto kern = from_table ? &round64_kernel<true> : &round64_kernel<false>;
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(hub_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kHubSmem));
     int rc = with_hub_kernel(sh, st, [&](cudaStream_t hs, int *hub_counter) {
       int hgrid = (int)std::min<int64_t>(sh->n_hub, kNumSMs);
-      hub_round64_kernel<<<hgrid, 256, kHubSmem, hs>>>(
+      hub_kern<<<hgrid, 256, kHubSmem, hs>>>(
           *sh, (const float *)theta4, (const float *)table, max_deg, (const float *)h_in,
           (float *)h_out, (float *)m_out, hub_counter, hot_rows, peers, npeers);
     }, &ss);
     if (rc) return rc;
-    round64_kernel<<<grid, 256, 0, st>>>(*sh, (const float *)theta4, (const float *)table,
-                                         max_deg, (const float *)h_in, (float *)h_out,
-                                         (float *)m_out, counter, hot_rows, peers, npeers);
+    kern<<<grid, 256, 0, st>>>(*sh, (const float *)theta4, (const float *)table, max_deg,
+                               (const float *)h_in, (float *)h_out, (float *)m_out, counter,
+                               hot_rows, peers, npeers);
     S2V_LAUNCH_CHECK();
     if (ss) S2V_CUDA_CHECK(cudaStreamWaitEvent(st, ss->done, 0));
     S2V_LAUNCH_CHECK();
@@ -895,6 +920,25 @@ int s2v_embed_round_peers(s2v_dtype dt, const s2v_shard *sh, const void *theta4,
     return fail(S2V_EINVAL, "fused peer rounds need K = 64 fp32");
   return embed_round_t<float>(sh, theta4, table, K, max_deg, h_in, h_out, m_out,
                               as_stream(stream), (float *const *)peer_outs, npeers);
+}
+
+int s2v_h1_table(s2v_dtype dt, const void *theta4, const void *table, int K, int max_deg,
+                 void *h1_table, void *stream) {
+  if (dt != S2V_F32 || K != 64) return fail(S2V_EINVAL, "h1 table needs K = 64 fp32");
+  if (max_deg < 0) return fail(S2V_EINVAL, "bad h1 table args");
+  const int rows = max_deg + 2;
+  h1_table_kernel<<<(rows * 64 + 255) / 256, 256, 0, as_stream(stream)>>>(
+      (const float *)theta4, (const float *)table, rows, (float *)h1_table);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_embed_round2_table(s2v_dtype dt, const s2v_shard *sh, const void *theta4,
+                           const void *table, int K, int max_deg, const void *h1_table,
+                           void *h_out, void *m_out, void *stream) {
+  if (dt != S2V_F32) return fail(S2V_EINVAL, "degree-table rounds need K = 64 fp32 at P = 1");
+  return embed_round_t<float>(sh, theta4, table, K, max_deg, h1_table, h_out, m_out,
+                              as_stream(stream), nullptr, 0, true);
 }
 
 int s2v_embed_round(s2v_dtype dt, const s2v_shard *sh, const void *theta4, const void *table,

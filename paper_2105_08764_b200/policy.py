@@ -19,6 +19,7 @@ accumulation order for it is not a simple chain; it costs one
 from __future__ import annotations
 
 import ctypes
+import os
 import struct
 from dataclasses import dataclass
 from pathlib import Path
@@ -244,9 +245,18 @@ def _allgather_rows(state: PartitionedState, comm, h: torch.Tensor, k: int, tag:
     comm.record(tag, state.rows_max * k * state.batch)
 
 
-# bench hook: when a list, every non-trivial round appends (start, end) CUDA
-# events recorded on the launching stream around its kernel
+# bench hook: when a list, every round that gathers neighbour rows of the
+# previous round from HBM appends (start, end) CUDA events recorded on the
+# launching stream around its kernel (the degree-table round 2 is not one)
 ROUND_TIMER = None
+
+
+def _degree_table_round2(state: PartitionedState, k: int, dt: int, num_layers: int) -> bool:
+    """Round 2 from the per-degree table of round-1 outputs (s2v_h1_table +
+    s2v_embed_round2_table): K = 64 fp32 at P = 1.  S2V_DEG_TABLE=0 turns it
+    off (the plain round reading h1 gives the same bits)."""
+    return (state.world == 1 and k == 64 and dt == _lib.S2V_F32 and num_layers >= 2
+            and os.environ.get("S2V_DEG_TABLE", "1") != "0")
 
 
 def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers: int, comm,
@@ -272,9 +282,25 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
         ms = None
     h_prev = None
     out = []
+    h1t = None
+    if _degree_table_round2(state, k, dt, num_layers):
+        h1t = state.workspace("h1t", (k, max_deg), lambda: torch.empty(
+            (max_deg + 2) * k, dtype=torch.float32, device=state.device))
+        _lib.call("s2v_h1_table", dt, dparams.ptr("theta4"), ptr(table), k, max_deg, ptr(h1t),
+                  st)
     for layer in range(num_layers):
         h_out = hs[layer] if tape else hs[layer % 2]
         m_out = ms[layer] if (tape and layer > 0) else None
+        if h1t is not None and layer == 0 and not tape:
+            # inference: nothing reads h1 but round 2, which reads the table
+            out.append(None)
+            continue
+        if h1t is not None and layer == 1:
+            _lib.call("s2v_embed_round2_table", dt, state.shard_ref(), dparams.ptr("theta4"),
+                      ptr(table), k, max_deg, ptr(h1t), ptr(h_out), ptr(m_out), st)
+            h_prev = h_out
+            out.append(h_out)
+            continue
         timer = ROUND_TIMER if (ROUND_TIMER is not None and h_prev is not None) else None
         if timer is not None:
             ev0 = torch.cuda.Event(enable_timing=True)

@@ -61,3 +61,34 @@ def test_hub_rows_bitwise_vs_oracle(make):
     assert np.array_equal(cand_gpu, cand)
     assert np.array_equal(h_gpu, h)
     assert np.array_equal(s_gpu, sc)
+
+
+@pytest.mark.parametrize("make", ["ba", "hub"])
+def test_degree_table_round2_equals_plain_round(make, monkeypatch):
+    """Round 2 from the per-degree table of round-1 outputs
+    (s2v_embed_round2_table) gives the bits of the plain round reading h1,
+    for a batch of slots with partial solutions, with and without hub rows."""
+    gs = [_hub_graph(), P.generate_ba(6000, 4, 9)] if make == "hub" else \
+        [P.generate_ba(4000, 6, 1), P.generate_ba(4000, 3, 2), P.generate_ba(4000, 8, 3)]
+    n = gs[0].num_nodes
+    params = P.PolicyParams.initialize(64, 5, seed=3)
+    rng = np.random.default_rng(4)
+    sol = (rng.random((len(gs), n)) < 0.1).astype(np.uint8)
+
+    def run():
+        def worker(comm):
+            part = P.partition_rows(n, 1)[0]
+            st = P.PartitionedState(gs, part, solutions=sol)
+            emb = P.embed_forward(st, params, comm)
+            return np.asarray(emb).copy(), P.q_forward(emb, st.cand, params, comm)
+        return P.run_workers(1, worker)[0]
+
+    monkeypatch.setenv("S2V_DEG_TABLE", "1")
+    h_t, s_t = run()
+    monkeypatch.setenv("S2V_DEG_TABLE", "0")
+    h_p, s_p = run()
+    assert np.array_equal(h_t, h_p)
+    assert np.array_equal(s_t, s_p)
+    rp, cols = gs[1].csr_arrays()
+    h_o = cref.forward(rp, cols, sol[1], params.as_dict(), 5)[0]
+    assert np.array_equal(h_t[1].T, h_o)  # (scores at B > 1 follow the batched u1 order)
