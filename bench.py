@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg1 / cfg5 legs")
     ap.add_argument("--rmat-scale", type=int, default=22)
+    ap.add_argument("--full-episode", action="store_true",
+                    help="also time a full adaptive solve of the R-MAT graph (configs[4]); "
+                         "takes minutes")
     ap.add_argument("--same-device", action="store_true",
                     help="bind every rank to cuda:0 (multi-process test on one GPU)")
     return ap.parse_args()
@@ -500,6 +503,12 @@ def main():
                          "(a,b,c = .57,.19,.19, seed 0), K=64, T=5, first steps of the adaptive "
                          "episode (BASELINE configs[4])")
         leg5["graph_gen_s"] = round(time.time() - t0, 2)
+        if args.full_episode and world == 1:
+            t_solve, res = full_solve_leg(P, comm, g5)
+            leg5["full_adaptive_solve_s"] = t_solve
+            leg5["full_solve_cover"] = res.cover_size
+            leg5["full_solve_evals"] = res.policy_evals
+            leg5["full_solve_skipped"] = res.skipped
         extra.append(leg5)
 
     if rank == 0:

@@ -72,6 +72,20 @@ typedef struct {
                               rows (degree > S2V_HUB_DEGREE) first, then the
                               rest, each by descending degree; NULL = identity */
   int64_t n_hub;           /* rows handled by the CTA-cooperative hub kernel */
+  const int32_t *active;   /* NULL, or the active-row list (B = 1, P = 1): a
+                              stable subsequence of `order` holding every row
+                              with rdeg > 0 (s2v_active_compact); the
+                              forward rounds and the scorer then visit only
+                              these rows (rows with rdeg = 0 keep the
+                              constant h1_table row, see s2v_colsum_residual) */
+  const int64_t *active_n; /* [2] device: rows in `active`, hub rows at its head */
+  const int64_t *active_ptr;  /* NULL, or the compact CSR of the active list
+                                 (s2v_active_compact): list position j has
+                                 the entries active_cols[active_ptr[j] ..
+                                 active_ptr[j+1]) -- the row's entries alive
+                                 when it was built; one that died since has
+                                 an endpoint in S, so rounds test sol[nbr] */
+  const uint32_t *active_cols;
 } s2v_shard;
 
 #define S2V_HUB_DEGREE 4096
@@ -145,12 +159,38 @@ int s2v_embed_round2_table(s2v_dtype dt, const s2v_shard *sh, const void *theta4
                            const void *table, int K, int max_deg, const void *h1_table,
                            void *h_out, void *m_out, void *stream);
 
+/* Stable in-place compaction of an active-row list: keeps the rows of
+ * list[0, n[0]) with rdeg > 0, in order, and updates n = {rows, rows among
+ * the first n[1] (hub rows)}.  With row_ptr_out ([cap+1]) and cols_out
+ * ([nnz]) it also writes the compact CSR of the kept rows (their alive
+ * entries, in order, indexed by list position) for s2v_shard.active_ptr /
+ * active_cols.  `cap` bounds n[0] (host-side capacity of
+ * list, tmp); ws holds s2v_active_workspace(cap) int64.  The rows dropped
+ * never come back: a residual degree only decreases during an episode
+ * (state.py:173-208).  B = 1, P = 1. */
+int s2v_active_compact(const s2v_shard *sh, int32_t *list, int64_t *n, int32_t *tmp,
+                       int64_t *ws, int64_t cap, int64_t *row_ptr_out, uint32_t *cols_out,
+                       void *stream);
+int64_t s2v_active_workspace(int64_t cap);
+
 /* g[b][k] = numpy pairwise sum over the N nodes of slot b of h[.,k]; h must
  * hold every rank's rows (after an all-gather when P>1).  Replaces
  * embed.sum(axis=2) + q_fwd all-reduce (policy.py:199-200). */
 int s2v_colsum(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, void *g,
                void *workspace, size_t workspace_bytes, void *stream);
 size_t s2v_colsum_workspace(const s2v_shard *sh, int K, int elem_bytes);
+/* The same sums, reading h only for rows with rdeg > 0: a row with no alive
+ * neighbour has m = 0 in every round, so its final embedding is the round-1
+ * row h1_table[sol ? max_deg + 1 : 0] (s2v_h1_table) whatever h holds for
+ * it -- rows outside the active list are never written.  P = 1.
+ * Incremental (last != NULL, K = 64, [B*N] bytes kept between calls with the
+ * same workspace and h1_table): a row only ever turns dead, so a pairwise
+ * leaf whose rows are all dead now and were all dead at the previous call
+ * keeps the leaf sum left in the workspace; full = 1 recomputes every leaf
+ * (first call). */
+int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
+                        const void *h1_table, int max_deg, void *g, void *workspace,
+                        size_t workspace_bytes, uint8_t *last, int full, void *stream);
 
 /* Scores of this rank's rows: u2 = theta6 (h*cand), r = relu([u1;u2]),
  * score = sum_j fl(r_j theta7_j) (policy.py:201-207), masked selection keys

@@ -43,6 +43,10 @@ class s2v_shard(ctypes.Structure):
         ("residual", ctypes.c_void_p),
         ("order", ctypes.c_void_p),
         ("n_hub", ctypes.c_int64),
+        ("active", ctypes.c_void_p),
+        ("active_n", ctypes.c_void_p),
+        ("active_ptr", ctypes.c_void_p),
+        ("active_cols", ctypes.c_void_p),
     ]
 
 
@@ -67,6 +71,9 @@ _SIGNATURES = {
     "s2v_embed_round_peers": ([_I, _SH, _P, _P, _I, _I, _P, _P, _P, _I, _P, _P], _I),
     "s2v_colsum": ([_I, _SH, _I, _P, _P, _P, _SZ, _P], _I),
     "s2v_colsum_workspace": ([_SH, _I, _I], _SZ),
+    "s2v_colsum_residual": ([_I, _SH, _I, _P, _P, _I, _P, _P, _SZ, _P, _I, _P], _I),
+    "s2v_active_compact": ([_SH, _P, _P, _P, _P, _I64, _P, _P, _P], _I),
+    "s2v_active_workspace": ([_I64], _I64),
     "s2v_score": ([_I, _SH, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P], _I),
     "s2v_score_blocks": ([_SH], _I),
     "s2v_topk_merge": ([_SH, _P, _I, _P, _P], _I),

@@ -157,15 +157,17 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
   __shared__ int32_t s_rows[kTileRows];
   __shared__ int64_t s_e0[kTileRows], s_e1[kTileRows];  // neighbour range, empty if in S
   __shared__ int s_tile;
-  for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x)
-    thT[idx % 64][idx / 64] = theta4[idx];
+  bool have_theta = false;  // staged with the first tile (idle CTAs skip it)
   const int tid = threadIdx.x;
   const int hw = tid >> 4, sub = tid & 15;  // half-warp id, lane in half-warp
   const unsigned hmask = (tid & 16) ? 0xFFFF0000u : 0x0000FFFFu;
   const int hbase = tid & 16;
   const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
-  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
-  const int64_t first = sh.order ? sh.n_hub : 0;  // hub rows: hub_round64_kernel
+  // rows visited: the active list when set (residual rows only), else every
+  // row in processing order; hub rows at the head go to hub_round64_kernel
+  const int32_t *list = sh.active ? sh.active : sh.order;
+  const int64_t nrows = sh.active ? sh.active_n[0] : (int64_t)sh.batch * sh.num_rows;
+  const int64_t first = sh.active ? sh.active_n[1] : (sh.order ? sh.n_hub : 0);
   const int64_t ntiles = (nrows - first + kTileRows - 1) / kTileRows;
   for (;;) {
     __syncthreads();
@@ -173,15 +175,20 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= ntiles) break;
+    if (!have_theta) {  // visible to the projection after the gather's barrier
+      for (int idx = tid; idx < 64 * 64; idx += blockDim.x) thT[idx % 64][idx / 64] = theta4[idx];
+      have_theta = true;
+    }
     if (tid < kTileRows) {
       // one pass loads every row's id, range and membership in S
       const int64_t q = first + tile * kTileRows + tid;
-      const int32_t r = q < nrows ? (sh.order ? sh.order[q] : (int32_t)q) : -1;
+      const int32_t r = q < nrows ? (list ? list[q] : (int32_t)q) : -1;
       s_rows[tid] = r;
       int64_t e0 = 0, e1 = 0;
       if (r >= 0 && h_in && !sh.sol[r]) {
-        e0 = sh.row_ptr[r];
-        e1 = sh.row_ptr[r + 1];
+        // the active list's compact CSR is indexed by list position
+        e0 = sh.active_ptr ? sh.active_ptr[q] : sh.row_ptr[r];
+        e1 = sh.active_ptr ? sh.active_ptr[q + 1] : sh.row_ptr[r + 1];
       }
       s_e0[tid] = e0;
       s_e1[tid] = e1;
@@ -194,8 +201,9 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       const int64_t r = s_rows[lr];
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       if (s_e1[lr] > s_e0[lr])
-        acc = gather_row64<TABLE>(s_e0[lr], s_e1[lr], sh.cols, h_in, sub, hmask, hbase,
-                                  hot_rows, pol_hot, pol_cold, sh.rdeg);
+        acc = gather_row64<TABLE>(s_e0[lr], s_e1[lr], sh.active_ptr ? sh.active_cols : sh.cols,
+                                  h_in, sub, hmask, hbase, hot_rows, pol_hot, pol_cold, sh.rdeg,
+                                  sh.active_ptr ? sh.sol : nullptr);
       *reinterpret_cast<float4 *>(&ms[lr][sub * 4]) = acc;
       if (m_out && r >= 0) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
     }
@@ -256,19 +264,28 @@ __global__ void __launch_bounds__(256, 1) hub_round64_kernel(
   float *mrow = hub_smem + 2 * kHubBatch * 64 + 64 * 65;
   __shared__ int s_q;
   const int tid = threadIdx.x, sub = tid & 15;
-  for (int idx = tid; idx < 64 * 64; idx += 256) thT[idx % 64][idx / 64] = theta4[idx];
   const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
+  bool have_theta = false;  // staged with the first row (idle CTAs skip it)
   for (;;) {
     __syncthreads();
     if (tid == 0) s_q = atomicAdd(counter, 1);
     __syncthreads();
     const int64_t q = s_q;
-    if (q >= sh.n_hub) break;
-    const int64_t r = sh.order[q];
+    if (q >= (sh.active ? sh.active_n[1] : sh.n_hub)) break;
+    if (!have_theta) {  // visible to the epilogue after the gather's barriers
+      for (int idx = tid; idx < 64 * 64; idx += 256) thT[idx % 64][idx / 64] = theta4[idx];
+      have_theta = true;
+    }
+    const int64_t r = sh.active ? sh.active[q] : sh.order[q];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (h_in && !sh.sol[r])
-      acc = hub_gather_row64<TABLE>(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, h_in, ring,
-                                    hot_rows, pol_hot, pol_cold, sh.rdeg);
+    if (h_in && !sh.sol[r]) {
+      if (sh.active_ptr)
+        acc = hub_gather_row64<TABLE>(sh.active_ptr[q], sh.active_ptr[q + 1], sh.active_cols,
+                                      h_in, ring, hot_rows, pol_hot, pol_cold, sh.rdeg, sh.sol);
+      else
+        acc = hub_gather_row64<TABLE>(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, h_in, ring,
+                                      hot_rows, pol_hot, pol_cold, sh.rdeg);
+    }
     if (tid < 16) {
       *reinterpret_cast<float4 *>(mrow + sub * 4) = acc;
       if (m_out) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
@@ -350,10 +367,30 @@ struct PairwiseCtx {
   const void *h;
   int64_t N, rows_max, base, extra;
   int32_t P, b, K;
+  // residual mode (P = 1): rows with rdeg = 0 read dead[sol ? K : 0 .. + K)
+  const void *dead;
+  const int32_t *rdeg;
+  const uint8_t *sol;
+  // incremental residual mode: last[row] = the row's class at the previous
+  // call (0 live, 1/2 dead); a leaf dead now and then keeps its value
+  uint8_t *last;
+  int full;
 };
+
+__device__ __forceinline__ int64_t phys_node(const PairwiseCtx &c, int64_t u) {
+  if (c.P == 1) return (int64_t)c.b * c.rows_max + u;
+  const int64_t big = c.extra * (c.base + 1);
+  const int64_t r = u < big ? u / (c.base + 1) : c.extra + (u - big) / c.base;
+  const int64_t start = r * c.base + (r < c.extra ? r : c.extra);
+  return ((int64_t)c.b * c.P + r) * c.rows_max + (u - start);
+}
 
 template <class T>
 __device__ __forceinline__ T load_node(const PairwiseCtx &c, int64_t u, int k) {
+  if (c.dead) {
+    const int64_t r = (int64_t)c.b * c.N + u;
+    if (c.rdeg[r] == 0) return reinterpret_cast<const T *>(c.dead)[(c.sol[r] ? c.K : 0) + k];
+  }
   int64_t phys;
   if (c.P == 1) {
     phys = (int64_t)c.b * c.rows_max + u;
@@ -401,6 +438,97 @@ __global__ void __launch_bounds__(256) colsum_leaf_kernel(PairwiseCtx c,
   }
 }
 
+// K = 64: one block of 512 threads per (leaf, slot), k = tid & 63 and
+// accumulator j = tid >> 6.  In residual mode the leaf's rows are classified
+// once into shared memory (0 = read h, 1/2 = dead row with sol 0/1), so the
+// 64 x 8 chains read rdeg/sol from HBM once per row and h only for live rows.
+template <class T>
+__global__ void __launch_bounds__(512) colsum_leaf64_kernel(PairwiseCtx c,
+                                                            const int64_t *__restrict__ leaves,
+                                                            int64_t nvals, T *__restrict__ vals) {
+  __shared__ T part[8][64];
+  __shared__ T s_dead[2][64];
+  __shared__ uint8_t s_code[128];
+  c.b = blockIdx.y;
+  const int leaf = blockIdx.x, tid = threadIdx.x;
+  const int k = tid & 63, j = tid >> 6;
+  const int64_t u0 = leaves[2 * leaf], n = leaves[2 * leaf + 1];
+  const T *h = reinterpret_cast<const T *>(c.h);
+  const bool res = c.dead != nullptr;
+  if (res) {
+    bool live = false;
+    if (tid < n) {
+      const int64_t r = (int64_t)c.b * c.N + u0 + tid;
+      const uint8_t code = c.rdeg[r] == 0 ? (c.sol[r] ? 2 : 1) : 0;
+      s_code[tid] = code;
+      live = code == 0;
+      if (c.last) {  // a row only ever goes live -> dead (rdeg never grows)
+        live |= c.last[r] == 0;
+        c.last[r] = code;
+      }
+    }
+    if (tid < 128) s_dead[tid >> 6][k] = reinterpret_cast<const T *>(c.dead)[tid];
+    // every row dead now and at the previous call: the cached value stands
+    if (!__syncthreads_or(live || c.full || !c.last)) return;
+  }
+  // generic pointer to row i's value: a dead row's lives in shared memory
+  auto src = [&](int64_t i) -> const T * {
+    if (res) {
+      const int code = s_code[i];
+      if (code) return &s_dead[code - 1][k];
+    }
+    return h + phys_node(c, u0 + i) * 64 + k;
+  };
+  auto val = [&](int64_t i) -> T { return *src(i); };
+  if (n >= 8) {
+    // all 16 loads of the chain issued before the sequential adds
+    const int stop = (int)(n - (n % 8));
+    T v[16];
+#pragma unroll
+    for (int t = 0; t < 16; t++) v[t] = (8 * t + j < stop) ? *src(8 * t + j) : T(0);
+    T r = v[0];
+#pragma unroll
+    for (int t = 1; t < 16; t++)
+      if (8 * t + j < stop) r = addT(r, v[t]);
+    part[j][k] = r;
+  }
+  __syncthreads();
+  if (j == 0) {
+    T out;
+    int64_t i;
+    if (n < 8) {
+      out = T(0);
+      i = 0;
+    } else {
+      out = addT(addT(addT(part[0][k], part[1][k]), addT(part[2][k], part[3][k])),
+                 addT(addT(part[4][k], part[5][k]), addT(part[6][k], part[7][k])));
+      i = n - (n % 8);
+    }
+    for (; i < n; i++) out = addT(out, val(i));
+    vals[((int64_t)c.b * nvals + leaf) * 64 + k] = out;
+  }
+}
+
+// Every internal node of height >= first_level in one CTA (the top of the
+// tree: few nodes per height), heights separated by __syncthreads.
+template <class T>
+__global__ void __launch_bounds__(1024) colsum_top_kernel(const int32_t *__restrict__ left,
+                                                          const int32_t *__restrict__ right,
+                                                          const int *__restrict__ lvl, int nlvl,
+                                                          int nleaves, int64_t nvals, int K,
+                                                          T *__restrict__ vals) {
+  T *v = vals + (int64_t)blockIdx.x * nvals * K;
+  for (int l = 0; l < nlvl; l++) {
+    const int a = lvl[l], bnd = lvl[l + 1];
+    for (int e = threadIdx.x; e < (bnd - a) * K; e += blockDim.x) {
+      const int q = a + e / K, k = e % K;
+      v[(int64_t)(nleaves + q) * K + k] =
+          addT(v[(int64_t)left[q] * K + k], v[(int64_t)right[q] * K + k]);
+    }
+    __syncthreads();
+  }
+}
+
 // vals[b][base + q] = vals[b][left[q]] + vals[b][right[q]] for q in [0, count)
 template <class T>
 __global__ void colsum_level_kernel(const int32_t *__restrict__ left,
@@ -428,6 +556,7 @@ struct PairwisePlan {
   int32_t *d_left = nullptr, *d_right = nullptr;  // internal nodes, by height
   int nleaves = 0, ninternal = 0, root = 0;
   std::vector<int> level_start;  // internal index ranges per height
+  int *d_level_start = nullptr;  // the same ranges on the device
 };
 
 // returns (node id, height); ids < nleaves are leaves, internal nodes get
@@ -484,6 +613,9 @@ static int get_plan(int64_t N, PairwisePlan **out) {
       }
     }
     p.level_start.push_back((int)internal.size());
+    S2V_CUDA_CHECK(cudaMalloc(&p.d_level_start, sizeof(int) * p.level_start.size()));
+    S2V_CUDA_CHECK(cudaMemcpy(p.d_level_start, p.level_start.data(),
+                              sizeof(int) * p.level_start.size(), cudaMemcpyHostToDevice));
     p.root = rootp.second ? newid[rootp.first] : rootp.first;
     S2V_CUDA_CHECK(cudaMalloc(&p.d_leaves, sizeof(int64_t) * leaves.size()));
     S2V_CUDA_CHECK(cudaMemcpy(p.d_leaves, leaves.data(), sizeof(int64_t) * leaves.size(),
@@ -504,7 +636,8 @@ static int get_plan(int64_t N, PairwisePlan **out) {
 
 template <class T>
 static int colsum_t(const s2v_shard *sh, int K, const void *h, void *g, void *workspace,
-                    size_t workspace_bytes, cudaStream_t st) {
+                    size_t workspace_bytes, cudaStream_t st, const T *dead = nullptr,
+                    uint8_t *last = nullptr, int full = 1) {
   PairwisePlan *plan = nullptr;
   int rc = get_plan(sh->num_nodes, &plan);
   if (rc) return rc;
@@ -521,16 +654,37 @@ static int colsum_t(const s2v_shard *sh, int K, const void *h, void *g, void *wo
   c.extra = sh->num_nodes % sh->world;
   c.K = K;
   c.b = 0;
-  dim3 lgrid(plan->nleaves, (K + 31) / 32, sh->batch);
-  colsum_leaf_kernel<T><<<lgrid, dim3(32, 8), 0, st>>>(c, plan->d_leaves, nvals, vals);
+  c.dead = dead;
+  c.rdeg = sh->rdeg;
+  c.sol = sh->sol;
+  c.last = last;
+  c.full = full;
+  if (last && K != 64) return fail(S2V_EINVAL, "incremental colsum needs K = 64");
+  if (K == 64) {
+    colsum_leaf64_kernel<T><<<dim3(plan->nleaves, sh->batch), 512, 0, st>>>(c, plan->d_leaves,
+                                                                            nvals, vals);
+  } else {
+    dim3 lgrid(plan->nleaves, (K + 31) / 32, sh->batch);
+    colsum_leaf_kernel<T><<<lgrid, dim3(32, 8), 0, st>>>(c, plan->d_leaves, nvals, vals);
+  }
   S2V_LAUNCH_CHECK();
-  for (size_t lv = 0; lv + 1 < plan->level_start.size(); lv++) {
+  const int nlv = (int)plan->level_start.size() - 1;
+  int lv = 0;
+  // wide heights: one launch each; the rest (<= 512 nodes per height): one CTA
+  for (; lv < nlv; lv++) {
     const int a = plan->level_start[lv], bnd = plan->level_start[lv + 1];
     const int count = bnd - a;
+    if (count <= 512) break;
     int64_t work = (int64_t)count * K;
     int blocks = (int)std::min<int64_t>((work + 255) / 256, kNumSMs * 8);
     colsum_level_kernel<T><<<dim3(blocks, sh->batch), 256, 0, st>>>(
         plan->d_left + a, plan->d_right + a, count, plan->nleaves + a, nvals, K, vals);
+    S2V_LAUNCH_CHECK();
+  }
+  if (lv < nlv) {
+    colsum_top_kernel<T><<<sh->batch, 1024, 0, st>>>(plan->d_left, plan->d_right,
+                                                     plan->d_level_start + lv, nlv - lv,
+                                                     plan->nleaves, nvals, K, vals);
     S2V_LAUNCH_CHECK();
   }
   colsum_out_kernel<T><<<sh->batch, 64, 0, st>>>(plan->root, nvals, K, vals, (T *)g);
@@ -645,17 +799,23 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
     const uint8_t *__restrict__ cand_override, int mode, float *__restrict__ scores,
     Key *__restrict__ block_keys, int64_t *__restrict__ counts) {
   __shared__ __align__(16) float th6T[64][68];           // th6T[p][k] = theta6[k][p]
-  // xs[row][p] = h[row][p]*c; after the projection the same storage holds
+  // xT[p][row] = h[row][p]*c; after the projection the same storage holds
   // prod[row][k] = fl(relu(u2) * theta7), and at the end the key lists
   __shared__ __align__(16) float xbuf[kScoreTile * 68];
-  float(*xs)[68] = reinterpret_cast<float(*)[68]>(xbuf);
+  float *xT = xbuf;  // [64 p][64 rows], 4-row groups swizzled
   float(*prod)[65] = reinterpret_cast<float(*)[65]>(xbuf);
   __shared__ float s_t7[64];
   __shared__ uint8_t s_c[kScoreTile];
+  __shared__ int32_t s_i[kScoreTile];
   __shared__ float s_s0;
   __shared__ unsigned long long s_count;
   Key *s_keys = reinterpret_cast<Key *>(xbuf);
   const int b = blockIdx.y, tid = threadIdx.x;
+  if (sh.active && (int64_t)blockIdx.x * kScoreRowsPerBlock >= sh.active_n[0]) {
+    // past the end of the active list: no rows, no keys
+    if (tid < kTopK) block_keys[((int64_t)b * gridDim.x + blockIdx.x) * kTopK + tid] = null_key();
+    return;
+  }
   for (int idx = tid; idx < 64 * 64; idx += 256) th6T[idx % 64][idx / 64] = theta6[idx];
   if (tid < 64) s_t7[tid] = theta7[64 + tid];
   if (tid == 0) {
@@ -668,8 +828,10 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
 #pragma unroll
   for (int q = 0; q < kTopK; q++) top[q] = null_key();
   unsigned long long cnt = 0;
+  // positions [i0, i1) of this block: local rows, or entries of the active
+  // list (B = 1) when set -- rows off the list have rdeg = 0, not candidates
   const int64_t i0 = (int64_t)blockIdx.x * kScoreRowsPerBlock;
-  const int64_t i1 = min(i0 + kScoreRowsPerBlock, sh.num_rows);
+  const int64_t i1 = min(i0 + kScoreRowsPerBlock, sh.active ? sh.active_n[0] : sh.num_rows);
   const int64_t base_r = (int64_t)b * sh.num_rows;
   const int64_t base_phys = ((int64_t)b * sh.world + sh.rank) * sh.rows_max;
   const int kq = tid & 15, rq = tid >> 4;
@@ -677,15 +839,19 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
   // the current tile is projected
   float4 pre[4];
   uint8_t pre_c[4];
+  int32_t pre_i[4];
   auto load_tile = [&](int64_t t0) {
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       const int e = tid + q * 256;
       const int row = e >> 4, k4 = e & 15;
-      const int64_t i = t0 + row;
+      const int64_t j = t0 + row;
       pre[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       pre_c[q] = 0;
-      if (t0 < i1 && i < i1) {
+      pre_i[q] = -1;
+      if (t0 < i1 && j < i1) {
+        const int64_t i = sh.active ? sh.active[j] : j;
+        pre_i[q] = (int32_t)i;
         pre_c[q] = cand_override ? cand_override[base_r + i] : sh.cand[base_r + i];
         pre[q] = ldg_f4_pol(h + (base_phys + i) * 64 + k4 * 4, l2_policy_first());
       }
@@ -700,13 +866,17 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
       const int e = tid + q * 256;
       const int row = e >> 4, k4 = e & 15;
       const float c = pre_c[q] ? 1.f : 0.f;
-      if (k4 == 0) s_c[row] = pre_c[q];
-      float4 x;
-      x.x = __fmul_rn(pre[q].x, c);
-      x.y = __fmul_rn(pre[q].y, c);
-      x.z = __fmul_rn(pre[q].z, c);
-      x.w = __fmul_rn(pre[q].w, c);
-      *reinterpret_cast<float4 *>(&xs[row][k4 * 4]) = x;
+      if (k4 == 0) {
+        s_c[row] = pre_c[q];
+        s_i[row] = pre_i[q];
+      }
+      // transposed, 4-row groups XOR-swizzled by (p >> 2) & 7: the
+      // projection reads 4 rows of one p as one float4 (2-way store conflicts)
+      const int rsw = row ^ ((k4 & 7) << 2);
+      xT[(k4 * 4 + 0) * 64 + rsw] = __fmul_rn(pre[q].x, c);
+      xT[(k4 * 4 + 1) * 64 + rsw] = __fmul_rn(pre[q].y, c);
+      xT[(k4 * 4 + 2) * 64 + rsw] = __fmul_rn(pre[q].z, c);
+      xT[(k4 * 4 + 3) * 64 + rsw] = __fmul_rn(pre[q].w, c);
     }
     __syncthreads();
     load_tile(t0 + kScoreTile);
@@ -718,9 +888,12 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
 #pragma unroll 4
     for (int p = 0; p < 64; p++) {
       const float4 t = *reinterpret_cast<const float4 *>(&th6T[p][kq * 4]);
+      const float4 x4 =
+          *reinterpret_cast<const float4 *>(&xT[p * 64 + ((rq * 4) ^ (((p >> 2) & 7) << 2))]);
+      const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
       for (int a = 0; a < 4; a++) {
-        const float xr = xs[rq * 4 + a][p];
+        const float xr = xv[a];
         acc[a][0] = __fmaf_rn(t.x, xr, acc[a][0]);
         acc[a][1] = __fmaf_rn(t.y, xr, acc[a][1]);
         acc[a][2] = __fmaf_rn(t.z, xr, acc[a][2]);
@@ -738,7 +911,7 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
       float sc = s_s0;
 #pragma unroll 16
       for (int k = 0; k < 64; k++) sc = __fadd_rn(sc, prod[tid][k]);
-      const int64_t i = t0 + tid;
+      const int64_t i = s_i[tid];
       scores[base_r + i] = sc;
       const bool c = s_c[tid] != 0;
       const bool finite = isfinite(sc);
@@ -788,7 +961,8 @@ __global__ void topk_below_kernel(s2v_shard sh, const Key *__restrict__ keys,
 }
 
 __global__ void topk_merge_kernel(const Key *__restrict__ block_keys, int nblk, int d,
-                                  Key *__restrict__ top_out) {
+                                  Key *__restrict__ top_out,
+                                  const int64_t *__restrict__ active_n) {
   extern __shared__ unsigned char smem_raw[];
   Key *s_keys = reinterpret_cast<Key *>(smem_raw);
   const int b = blockIdx.x;
@@ -796,7 +970,13 @@ __global__ void topk_merge_kernel(const Key *__restrict__ block_keys, int nblk, 
 #pragma unroll
   for (int q = 0; q < kTopK; q++) top[q] = null_key();
   const Key *src = block_keys + (int64_t)b * nblk * kTopK;
-  const int64_t total = (int64_t)nblk * kTopK;
+  // active-row list: only its first blocks hold keys (the rest are empty)
+  int used = nblk;
+  if (active_n) {
+    const int64_t act_blk = (active_n[0] + kScoreRowsPerBlock - 1) / kScoreRowsPerBlock;
+    if (act_blk < used) used = (int)act_blk;
+  }
+  const int64_t total = (int64_t)used * kTopK;
   int64_t idx = threadIdx.x;
   for (; idx + 3 * blockDim.x < total; idx += 4 * blockDim.x) {
     Key k0 = src[idx], k1 = src[idx + blockDim.x], k2 = src[idx + 2 * blockDim.x],
@@ -822,6 +1002,8 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
   if (nrows == 0) return S2V_OK;
   if (from_table && !(sizeof(T) == 4 && K == 64 && sh->world == 1 && !npeers))
     return fail(S2V_EINVAL, "degree-table rounds need K = 64 fp32 at P = 1");
+  if (sh->active && !(sizeof(T) == 4 && K == 64 && sh->world == 1 && sh->batch == 1))
+    return fail(S2V_EINVAL, "active-row lists need K = 64 fp32, B = 1, P = 1");
   if (sizeof(T) == 4 && K == 64) {
     static thread_local int *counter = nullptr;
     if (!counter) S2V_CUDA_CHECK(cudaMalloc(&counter, sizeof(int)));
@@ -880,6 +1062,16 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
 #undef S2V_LAUNCH_ROUND
   S2V_LAUNCH_CHECK();
   return S2V_OK;
+}
+
+// dead rows' embedding: rows sol ? max_deg+1 : 0 of the h1 table, packed
+template <class T>
+__global__ void dead_rows_kernel(const T *__restrict__ h1_table, int K, int max_deg,
+                                 T *__restrict__ dead) {
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    dead[k] = h1_table[k];
+    dead[K + k] = h1_table[(int64_t)(max_deg + 1) * K + k];
+  }
 }
 
 }  // namespace s2v
@@ -963,6 +1155,28 @@ int s2v_colsum(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, void *g,
   return colsum_t<double>(sh, K, h, g, workspace, workspace_bytes, as_stream(stream));
 }
 
+int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
+                        const void *h1_table, int max_deg, void *g, void *workspace,
+                        size_t workspace_bytes, uint8_t *last, int full, void *stream) {
+  if (sh->world != 1) return fail(S2V_EINVAL, "residual colsum needs P = 1");
+  if (max_deg < 0 || !h1_table) return fail(S2V_EINVAL, "bad residual colsum args");
+  cudaStream_t st = as_stream(stream);
+  const size_t elem = dt == S2V_F32 ? 4 : 8;
+  const size_t need = s2v_colsum_workspace(sh, K, (int)elem);
+  if (workspace_bytes < need + 2 * K * elem)
+    return fail(S2V_EINVAL, "residual colsum workspace too small");
+  void *dead = (char *)workspace + need;  // after the tree values
+  if (dt == S2V_F32) {
+    dead_rows_kernel<float><<<1, 64, 0, st>>>((const float *)h1_table, K, max_deg, (float *)dead);
+    S2V_LAUNCH_CHECK();
+    return colsum_t<float>(sh, K, h, g, workspace, need, st, (const float *)dead, last, full);
+  }
+  dead_rows_kernel<double><<<1, 64, 0, st>>>((const double *)h1_table, K, max_deg,
+                                             (double *)dead);
+  S2V_LAUNCH_CHECK();
+  return colsum_t<double>(sh, K, h, g, workspace, need, st, (const double *)dead, last, full);
+}
+
 int s2v_score_blocks(const s2v_shard *sh) {
   int64_t n = (sh->num_rows + kScoreRowsPerBlock - 1) / kScoreRowsPerBlock;
   return (int)(n < 1 ? 1 : n);
@@ -972,6 +1186,8 @@ int s2v_score(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, const voi
               const void *theta6, const void *theta7, const uint8_t *cand_override, int mode,
               void *scores, uint64_t *block_keys, int64_t *counts, void *stream) {
   if (K > 256) return fail(S2V_EINVAL, "embed_dim %d > 256 unsupported", K);
+  if (sh->active && !(dt == S2V_F32 && K == 64 && sh->world == 1 && sh->batch == 1))
+    return fail(S2V_EINVAL, "active-row lists need K = 64 fp32, B = 1, P = 1");
   cudaStream_t st = as_stream(stream);
   S2V_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(int64_t) * sh->batch, st));
   dim3 grid(s2v_score_blocks(sh), sh->batch);
@@ -1040,8 +1256,8 @@ int s2v_topk_merge(const s2v_shard *sh, const uint64_t *block_keys, int d, uint6
   size_t smem = sizeof(Key) * 256 * kTopK;
   S2V_CUDA_CHECK(cudaFuncSetAttribute(topk_merge_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  topk_merge_kernel<<<sh->batch, 256, smem, as_stream(stream)>>>((const Key *)block_keys, nblk,
-                                                                  d, (Key *)top);
+  topk_merge_kernel<<<sh->batch, 256, smem, as_stream(stream)>>>(
+      (const Key *)block_keys, nblk, d, (Key *)top, sh->active ? sh->active_n : nullptr);
   S2V_LAUNCH_CHECK();
   return S2V_OK;
 }

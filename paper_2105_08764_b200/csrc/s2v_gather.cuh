@@ -50,9 +50,14 @@ __device__ __forceinline__ void add4(float4 &a, const float4 &b) {
 // h_in.  TABLE = true (round 2 at P = 1): h_in is the 1-row-per-degree table
 // of round-1 outputs and the source row is the neighbour's residual degree
 // (an alive neighbour is never in S, so its round-1 row is table[rdeg]).
+// sol_of (compact CSR of an active list): an entry built alive has died
+// since iff its neighbour entered S.
 template <bool TABLE>
-__device__ __forceinline__ uint32_t source_row(uint32_t c, const int32_t *__restrict__ deg_of) {
-  if (!TABLE || (c & S2V_DEAD)) return c;
+__device__ __forceinline__ uint32_t source_row(uint32_t c, const int32_t *__restrict__ deg_of,
+                                               const uint8_t *__restrict__ sol_of) {
+  if (c & S2V_DEAD) return c;
+  if (sol_of && sol_of[c]) return S2V_DEAD;
+  if (!TABLE) return c;
   return (uint32_t)__ldg(deg_of + c);
 }
 
@@ -64,12 +69,13 @@ __device__ __forceinline__ float4 gather_row64(int64_t e, const int64_t e1,
                                                const float *__restrict__ h_in, int sub,
                                                unsigned hmask, int hbase, uint32_t hot_rows,
                                                uint64_t pol_hot, uint64_t pol_cold,
-                                               const int32_t *__restrict__ deg_of = nullptr) {
+                                               const int32_t *__restrict__ deg_of = nullptr,
+                                               const uint8_t *__restrict__ sol_of = nullptr) {
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (; e < e1; e += 16) {
     const int cnt = (e1 - e) < 16 ? (int)(e1 - e) : 16;
     const uint32_t mine = source_row<TABLE>(
-        sub < cnt ? ldg_u32_pol(cols + e + sub, pol_cold) : S2V_DEAD, deg_of);
+        sub < cnt ? ldg_u32_pol(cols + e + sub, pol_cold) : S2V_DEAD, deg_of, sol_of);
 #pragma unroll
     for (int half = 0; half < 2; half++) {
       if (half * 8 >= cnt) break;
@@ -110,12 +116,13 @@ __device__ __forceinline__ void hub_stage(int64_t e_batch, const int64_t e1,
                                           const float *__restrict__ src, float *buf /*[120][64]*/,
                                           int hw, int sub, unsigned hmask, int hbase,
                                           uint32_t hot_rows, uint64_t pol_hot, uint64_t pol_cold,
-                                          const int32_t *__restrict__ deg_of) {
+                                          const int32_t *__restrict__ deg_of,
+                                          const uint8_t *__restrict__ sol_of) {
   if (hw == 0) return;
   const int64_t base = e_batch + (int64_t)(hw - 1) * 8;
   const uint32_t mine = source_row<TABLE>(
       (sub < 8 && base + sub < e1) ? ldg_u32_pol(cols + base + sub, pol_cold) : S2V_DEAD,
-      deg_of);
+      deg_of, sol_of);
   float4 v[8];
 #pragma unroll
   for (int q = 0; q < 8; q++) {
@@ -135,7 +142,8 @@ __device__ __forceinline__ float4 hub_gather_row64(const int64_t e0, const int64
                                                    const float *__restrict__ src,
                                                    float *ring /*[2][120][64]*/, uint32_t hot_rows,
                                                    uint64_t pol_hot, uint64_t pol_cold,
-                                                   const int32_t *__restrict__ deg_of = nullptr) {
+                                                   const int32_t *__restrict__ deg_of = nullptr,
+                                                   const uint8_t *__restrict__ sol_of = nullptr) {
   const int tid = threadIdx.x, hw = tid >> 4, sub = tid & 15;
   const unsigned hmask = (tid & 16) ? 0xFFFF0000u : 0x0000FFFFu;
   const int hbase = tid & 16;
@@ -143,13 +151,13 @@ __device__ __forceinline__ float4 hub_gather_row64(const int64_t e0, const int64
   const int64_t nb = (e1 - e0 + kHubBatch - 1) / kHubBatch;
   if (nb > 0)
     hub_stage<TABLE>(e0, e1, cols, src, ring, hw, sub, hmask, hbase, hot_rows, pol_hot, pol_cold,
-                     deg_of);
+                     deg_of, sol_of);
   __syncthreads();
   for (int64_t b = 0; b < nb; b++) {
     if (b + 1 < nb)
       hub_stage<TABLE>(e0 + (b + 1) * kHubBatch, e1, cols, src,
                        ring + ((b + 1) & 1) * kHubBatch * 64, hw, sub, hmask, hbase, hot_rows,
-                       pol_hot, pol_cold, deg_of);
+                       pol_hot, pol_cold, deg_of, sol_of);
     if (hw == 0) {
       const float *cur = ring + (b & 1) * kHubBatch * 64;
       const int64_t left = e1 - e0 - b * kHubBatch;

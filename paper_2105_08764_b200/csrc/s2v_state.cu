@@ -5,6 +5,7 @@
 //   PartitionedState.__init__ residual mask / degrees   pkg/src/graphrl/state.py:89-111
 //   PartitionedState.apply_action                       pkg/src/graphrl/state.py:173-208
 //   _solve_batch group loop with mid-group skip         pkg/src/graphrl/inference.py:125-146
+#include <algorithm>
 #include <cstdarg>
 #include <mutex>
 
@@ -220,6 +221,167 @@ __global__ void apply_phase3_kernel(s2v_shard sh, const int64_t *picks, int d,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Active-row list compaction (B = 1, P = 1): keep rows with rdeg > 0, stable.
+// 4096 list entries per CTA (16 consecutive per thread): count, then scatter
+// at the prefix of the CTA counts, then copy back.  Optionally the compact
+// CSR of the kept rows: row_ptr over list positions (prefix of rdeg -- the
+// alive entries of a row), then one warp per row copies its alive entries.
+// ws: [nchunks rows][nchunks hub rows][nchunks entries][rows, hub rows, entries]
+// ---------------------------------------------------------------------------
+constexpr int kCompactPer = 16;
+constexpr int kCompactChunk = 256 * kCompactPer;
+
+__device__ __forceinline__ int64_t block_sum_i64(int64_t v, int64_t *s_red /*[8]*/) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int64_t t = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s_red[w];
+  return t;
+}
+
+// exclusive prefix of v over the block (256 threads)
+__device__ __forceinline__ int64_t block_exscan_i64(int64_t v, int64_t *s_warp /*[8]*/) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t incl = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  __syncthreads();
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  int64_t before = 0;
+  for (int w = 0; w < warp; w++) before += s_warp[w];
+  return before + incl - v;
+}
+
+__global__ void __launch_bounds__(256) active_count_kernel(const int32_t *__restrict__ rdeg,
+                                                           const int32_t *__restrict__ list,
+                                                           const int64_t *__restrict__ n,
+                                                           int64_t *__restrict__ ws, int nchunks) {
+  __shared__ int64_t s_red[8];
+  const int64_t cnt = n[0], nh = n[1];
+  const int64_t j0 = (int64_t)blockIdx.x * kCompactChunk + threadIdx.x * kCompactPer;
+  int64_t a = 0, h = 0, e = 0;
+#pragma unroll
+  for (int t = 0; t < kCompactPer; t++) {
+    const int64_t j = j0 + t;
+    if (j < cnt) {
+      const int32_t d = rdeg[list[j]];
+      if (d > 0) {
+        a++;
+        e += d;
+        if (j < nh) h++;
+      }
+    }
+  }
+  a = block_sum_i64(a, s_red);
+  h = block_sum_i64(h, s_red);
+  e = block_sum_i64(e, s_red);
+  if (threadIdx.x == 0) {
+    ws[blockIdx.x] = a;
+    ws[nchunks + blockIdx.x] = h;
+    ws[2 * nchunks + blockIdx.x] = e;
+  }
+}
+
+__global__ void __launch_bounds__(256) active_scatter_kernel(
+    const int32_t *__restrict__ rdeg, const int32_t *__restrict__ list,
+    const int64_t *__restrict__ n, int64_t *__restrict__ ws, int nchunks,
+    int32_t *__restrict__ out, int64_t *__restrict__ row_ptr_out) {
+  __shared__ int64_t s_red[8];
+  const int tid = threadIdx.x;
+  int64_t off = 0, eoff = 0;
+  for (int c = tid; c < (int)blockIdx.x; c += 256) {
+    off += ws[c];
+    eoff += ws[2 * nchunks + c];
+  }
+  off = block_sum_i64(off, s_red);
+  eoff = block_sum_i64(eoff, s_red);
+  if (blockIdx.x == 0) {  // new totals, read by the copy-back kernel
+    int64_t a = 0, h = 0, e = 0;
+    for (int c = tid; c < nchunks; c += 256) {
+      a += ws[c];
+      h += ws[nchunks + c];
+      e += ws[2 * nchunks + c];
+    }
+    a = block_sum_i64(a, s_red);
+    h = block_sum_i64(h, s_red);
+    e = block_sum_i64(e, s_red);
+    if (tid == 0) {
+      ws[3 * nchunks] = a;
+      ws[3 * nchunks + 1] = h;
+      ws[3 * nchunks + 2] = e;
+    }
+  }
+  const int64_t cnt = n[0];
+  const int64_t j0 = (int64_t)blockIdx.x * kCompactChunk + tid * kCompactPer;
+  int32_t rows[kCompactPer], degs[kCompactPer];
+  int64_t mine = 0, mine_e = 0;
+#pragma unroll
+  for (int t = 0; t < kCompactPer; t++) {
+    const int64_t j = j0 + t;
+    rows[t] = j < cnt ? list[j] : -1;
+    degs[t] = rows[t] >= 0 ? rdeg[rows[t]] : 0;
+    if (degs[t] > 0) {
+      mine++;
+      mine_e += degs[t];
+    }
+  }
+  int64_t pos = off + block_exscan_i64(mine, s_red);
+  int64_t epos = eoff + block_exscan_i64(mine_e, s_red);
+#pragma unroll
+  for (int t = 0; t < kCompactPer; t++)
+    if (degs[t] > 0) {
+      out[pos] = rows[t];
+      if (row_ptr_out) row_ptr_out[pos] = epos;
+      pos++;
+      epos += degs[t];
+    }
+}
+
+__global__ void active_copy_kernel(const int32_t *__restrict__ tmp, const int64_t *__restrict__ ws,
+                                   int nchunks, int32_t *__restrict__ list,
+                                   int64_t *__restrict__ n, int64_t *__restrict__ row_ptr_out) {
+  const int64_t cnt = ws[3 * nchunks];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cnt;
+       j += (int64_t)gridDim.x * blockDim.x)
+    list[j] = tmp[j];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    n[0] = cnt;
+    n[1] = ws[3 * nchunks + 1];
+    if (row_ptr_out) row_ptr_out[cnt] = ws[3 * nchunks + 2];
+  }
+}
+
+// one warp per kept row: its alive entries, in order, at row_ptr_out[j]
+__global__ void __launch_bounds__(256) active_fill_kernel(s2v_shard sh,
+                                                          const int32_t *__restrict__ list,
+                                                          const int64_t *__restrict__ n,
+                                                          const int64_t *__restrict__ row_ptr_out,
+                                                          uint32_t *__restrict__ cols_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t cnt = n[0];
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < cnt;
+       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t r = list[j];
+    int64_t o = row_ptr_out[j];
+    const int64_t e1 = sh.row_ptr[r + 1];
+    for (int64_t e = sh.row_ptr[r]; e < e1; e += 32) {
+      const bool in = e + lane < e1;
+      const uint32_t c = in ? sh.cols[e + lane] : S2V_DEAD;
+      const bool alive = !(c & S2V_DEAD);
+      const unsigned m = __ballot_sync(0xffffffffu, alive);
+      if (alive) cols_out[o + __popc(m & ((1u << lane) - 1))] = c;
+      o += __popc(m);
+    }
+  }
+}
+
 }  // namespace s2v
 
 using namespace s2v;
@@ -268,6 +430,35 @@ int s2v_apply_phase2(const s2v_shard *sh, const int64_t *picks, int d, const int
   S2V_LAUNCH_CHECK();
   apply_phase3_kernel<<<grid, 256, 0, as_stream(stream)>>>(*sh, picks, d, applied);
   S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int64_t s2v_active_workspace(int64_t cap) {
+  return 3 * ((cap + kCompactChunk - 1) / kCompactChunk) + 3;
+}
+
+int s2v_active_compact(const s2v_shard *sh, int32_t *list, int64_t *n, int32_t *tmp,
+                       int64_t *ws, int64_t cap, int64_t *row_ptr_out, uint32_t *cols_out,
+                       void *stream) {
+  if (sh->batch != 1 || sh->world != 1)
+    return fail(S2V_EINVAL, "active-row lists need B = 1, P = 1");
+  if ((row_ptr_out == nullptr) != (cols_out == nullptr))
+    return fail(S2V_EINVAL, "compact CSR needs both row_ptr_out and cols_out");
+  if (cap <= 0) return S2V_OK;
+  cudaStream_t st = as_stream(stream);
+  const int nchunks = (int)((cap + kCompactChunk - 1) / kCompactChunk);
+  active_count_kernel<<<nchunks, 256, 0, st>>>(sh->rdeg, list, n, ws, nchunks);
+  S2V_LAUNCH_CHECK();
+  active_scatter_kernel<<<nchunks, 256, 0, st>>>(sh->rdeg, list, n, ws, nchunks, tmp, row_ptr_out);
+  S2V_LAUNCH_CHECK();
+  const int cgrid = (int)std::min<int64_t>((cap + 255) / 256, kNumSMs * 4);
+  active_copy_kernel<<<cgrid, 256, 0, st>>>(tmp, ws, nchunks, list, n, row_ptr_out);
+  S2V_LAUNCH_CHECK();
+  if (cols_out) {
+    const int fgrid = (int)std::min<int64_t>((cap + 7) / 8, kNumSMs * 8);
+    active_fill_kernel<<<fgrid, 256, 0, st>>>(*sh, list, n, row_ptr_out, cols_out);
+    S2V_LAUNCH_CHECK();
+  }
   return S2V_OK;
 }
 

@@ -260,17 +260,22 @@ def _degree_table_round2(state: PartitionedState, k: int, dt: int, num_layers: i
 
 
 def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers: int, comm,
-                    dtype, tape: bool):
+                    dtype, tape: bool, reuse_tables: bool = False):
     """L embedding rounds.  Returns the list of h buffers (all of them when
-    tape, else the final one) and, when tape, the m buffers per round."""
+    tape, else the final one) and, when tape, the m buffers per round.
+    reuse_tables: the e12 / h1 tables of this state were last built from
+    these same device parameters (an episode's later evaluations) -- skip
+    rebuilding them."""
     k = dparams.k
     dt = _dt_code(dtype)
     st = stream_ptr()
     max_deg = int(state.max_deg)
     table = state.workspace("e12", (k, np.dtype(dtype).str, max_deg), lambda: torch.empty(
         (max_deg + 2) * k, dtype=_torch_dtype(dtype), device=state.device))
-    _lib.call("s2v_e12_table", dt, dparams.ptr("theta1"), dparams.ptr("theta2"),
-              dparams.ptr("theta3"), k, max_deg, ptr(table), st)
+    reuse = reuse_tables and getattr(state, "_tables_of", None) is dparams
+    if not reuse:
+        _lib.call("s2v_e12_table", dt, dparams.ptr("theta1"), dparams.ptr("theta2"),
+                  dparams.ptr("theta3"), k, max_deg, ptr(table), st)
     if tape:
         hs = _buffers(state, k, dtype, num_layers)
         rows = state.batch * state.part.num_rows
@@ -286,8 +291,12 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
     if _degree_table_round2(state, k, dt, num_layers):
         h1t = state.workspace("h1t", (k, max_deg), lambda: torch.empty(
             (max_deg + 2) * k, dtype=torch.float32, device=state.device))
-        _lib.call("s2v_h1_table", dt, dparams.ptr("theta4"), ptr(table), k, max_deg, ptr(h1t),
-                  st)
+        if not reuse:
+            _lib.call("s2v_h1_table", dt, dparams.ptr("theta4"), ptr(table), k, max_deg,
+                      ptr(h1t), st)
+    elif state.active_on:
+        raise RuntimeError("active-row lists need the degree-table round (K = 64 fp32, P = 1)")
+    state._tables_of = dparams
     for layer in range(num_layers):
         h_out = hs[layer] if tape else hs[layer % 2]
         m_out = ms[layer] if (tape and layer > 0) else None
@@ -351,12 +360,33 @@ def _colsum_device(emb: DeviceEmbedding) -> torch.Tensor:
     st = emb.state
     k = emb.k
     wsb = _lib.load().s2v_colsum_workspace(st.shard_ref(), k, emb.dtype.itemsize)
+    wsb += 2 * k * emb.dtype.itemsize  # the two dead-row embeddings (residual mode)
     ws = st.workspace("colsum", (k, emb.dtype.str), lambda: {
         "ws": torch.empty(max(wsb // emb.dtype.itemsize, 1), dtype=_torch_dtype(emb.dtype),
                           device=st.device),
         "g": torch.empty(st.batch * k, dtype=_torch_dtype(emb.dtype), device=st.device)})
-    _lib.call("s2v_colsum", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h), ptr(ws["g"]),
-              ptr(ws["ws"]), wsb, stream_ptr())
+    if st.active_on:
+        # rows off the active list were never written this forward: they
+        # take their (constant) round-1 row from the h1 table; an episode
+        # keeps its own tree workspace so that all-dead leaves are reused
+        h1t = st.workspace("h1t", (k, int(st.max_deg)), None)
+        inc = st.colsum_cache
+        if inc is None:
+            _lib.call("s2v_colsum_residual", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h),
+                      ptr(h1t), int(st.max_deg), ptr(ws["g"]), ptr(ws["ws"]), wsb, None, 1,
+                      stream_ptr())
+        else:
+            if inc.get("ws") is None:
+                inc["ws"] = torch.empty_like(ws["ws"])
+                inc["last"] = torch.zeros(st.batch * st.num_nodes, dtype=torch.uint8,
+                                          device=st.device)
+            _lib.call("s2v_colsum_residual", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h),
+                      ptr(h1t), int(st.max_deg), ptr(ws["g"]), ptr(inc["ws"]), wsb,
+                      ptr(inc["last"]), 1 if inc["full"] else 0, stream_ptr())
+            inc["full"] = False
+    else:
+        _lib.call("s2v_colsum", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h),
+                  ptr(ws["g"]), ptr(ws["ws"]), wsb, stream_ptr())
     return ws["g"]
 
 
@@ -480,10 +510,11 @@ def decode_keys(top: np.ndarray):
 
 
 def evaluate_device(state: PartitionedState, params: PolicyParams, dparams, comm, d: int,
-                    mode: int = 0):
+                    mode: int = 0, reuse_tables: bool = False):
     """evaluate() without any host round trip (P = 1, device u1): returns the
     score workspace whose "out" holds counts [B] then top-d keys [B][d][2]."""
-    hs, _, _ = _forward_rounds(state, dparams, params.num_layers, comm, params.dtype, False)
+    hs, _, _ = _forward_rounds(state, dparams, params.num_layers, comm, params.dtype, False,
+                               reuse_tables=reuse_tables)
     emb = DeviceEmbedding(state, hs[-1], params.embed_dim, params.dtype, gathered=True)
     return _score(emb, params, dparams, None, mode, d, readback=False)
 

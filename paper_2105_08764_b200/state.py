@@ -18,6 +18,7 @@ after every mutation.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass
 
@@ -219,6 +220,32 @@ class PartitionedState:
 
     def shard_ref(self):
         return ctypes.byref(self._shard)
+
+    colsum_cache = None
+
+    @contextlib.contextmanager
+    def active_rows(self, rows: torch.Tensor, count: torch.Tensor, colsum_cache=None,
+                    csr=None):
+        """Within the block, forward rounds and the scorer visit only the rows
+        of the active list `rows` (int32, count[0] entries, count[1] hub rows
+        first; s2v_active_compact) -- the residual rows of an episode.
+        colsum_cache: the caller's dict for the incremental global sum
+        (s2v_colsum_residual with `last`), valid for fixed parameters.
+        csr: (row_ptr, cols) compact CSR of the list (s2v_active_compact)."""
+        sh = self._shard
+        sh.active, sh.active_n = ptr(rows), ptr(count)
+        if csr is not None:
+            sh.active_ptr, sh.active_cols = ptr(csr[0]), ptr(csr[1])
+        self.colsum_cache = colsum_cache
+        try:
+            yield
+        finally:
+            sh.active, sh.active_n, sh.active_ptr, sh.active_cols = None, None, None, None
+            self.colsum_cache = None
+
+    @property
+    def active_on(self) -> bool:
+        return bool(self._shard.active)
 
     def workspace(self, name: str, key, make):
         """Per-state cache of device scratch buffers (reused across steps)."""
