@@ -509,6 +509,82 @@ __global__ void __launch_bounds__(512) colsum_leaf64_kernel(PairwiseCtx c,
   }
 }
 
+// K = 64, 4 leaves per block of 256 threads: thread (leaf, k) runs all 8
+// accumulator chains of its column itself, so every row of the leaf is one
+// independent coalesced 256-byte load across the leaf's 64 threads (deep
+// memory-level parallelism, 8 waves at 2^22 rows instead of 55).  Residual
+// and incremental modes as colsum_leaf64_kernel.
+constexpr int kLeavesPerBlock = 4;
+
+template <class T>
+__global__ void __launch_bounds__(256) colsum_leaf64x4_kernel(PairwiseCtx c,
+                                                              const int64_t *__restrict__ leaves,
+                                                              int nleaves, int64_t nvals,
+                                                              T *__restrict__ vals) {
+  __shared__ T s_dead[2][64];
+  __shared__ uint8_t s_code[kLeavesPerBlock][128];
+  __shared__ int s_live[kLeavesPerBlock];
+  c.b = blockIdx.y;
+  const int tid = threadIdx.x, k = tid & 63, ll = tid >> 6;
+  const int leaf = blockIdx.x * kLeavesPerBlock + ll;
+  const bool ok = leaf < nleaves;
+  const int64_t u0 = ok ? leaves[2 * leaf] : 0, n = ok ? leaves[2 * leaf + 1] : 0;
+  const T *h = reinterpret_cast<const T *>(c.h);
+  const bool res = c.dead != nullptr;
+  if (res) {
+    if (tid < kLeavesPerBlock) s_live[tid] = (c.full || !c.last) ? 1 : 0;
+    if (tid < 128) s_dead[tid >> 6][k] = reinterpret_cast<const T *>(c.dead)[tid];
+    __syncthreads();
+    bool live = false;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; h2++) {  // the leaf's 64 threads classify its <= 128 rows
+      const int i = k + 64 * h2;
+      if (i < n) {
+        const int64_t r = (int64_t)c.b * c.N + u0 + i;
+        const uint8_t code = c.rdeg[r] == 0 ? (c.sol[r] ? 2 : 1) : 0;
+        s_code[ll][i] = code;
+        live |= code == 0;
+        if (c.last) {  // a row only ever goes live -> dead (rdeg never grows)
+          live |= c.last[r] == 0;
+          c.last[r] = code;
+        }
+      }
+    }
+    if (live) s_live[ll] = 1;
+    __syncthreads();
+    if (!s_live[ll]) return;  // all dead now and at the previous call
+  }
+  if (!ok) return;
+  auto src = [&](int64_t i) -> const T * {
+    if (res) {
+      const int code = s_code[ll][i];
+      if (code) return &s_dead[code - 1][k];
+    }
+    return h + phys_node(c, u0 + i) * 64 + k;
+  };
+  T out;
+  int64_t i = 0;
+  if (n < 8) {
+    out = T(0);
+  } else {
+    const int stop = (int)(n - (n % 8));
+    T r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = *src(j);
+    for (int base = 8; base < stop; base += 8) {
+      T v[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) v[j] = *src(base + j);
+#pragma unroll
+      for (int j = 0; j < 8; j++) r[j] = addT(r[j], v[j]);
+    }
+    out = addT(addT(addT(r[0], r[1]), addT(r[2], r[3])), addT(addT(r[4], r[5]), addT(r[6], r[7])));
+    i = stop;
+  }
+  for (; i < n; i++) out = addT(out, *src(i));
+  vals[((int64_t)c.b * nvals + leaf) * 64 + k] = out;
+}
+
 // Every internal node of height >= first_level in one CTA (the top of the
 // tree: few nodes per height), heights separated by __syncthreads.
 template <class T>
@@ -661,8 +737,17 @@ static int colsum_t(const s2v_shard *sh, int K, const void *h, void *g, void *wo
   c.full = full;
   if (last && K != 64) return fail(S2V_EINVAL, "incremental colsum needs K = 64");
   if (K == 64) {
-    colsum_leaf64_kernel<T><<<dim3(plan->nleaves, sh->batch), 512, 0, st>>>(c, plan->d_leaves,
-                                                                            nvals, vals);
+    static const bool x4 = [] {
+      const char *e = getenv("S2V_COLSUM_X4");
+      return !(e && e[0] == '0');
+    }();
+    if (x4)
+      colsum_leaf64x4_kernel<T>
+          <<<dim3((plan->nleaves + kLeavesPerBlock - 1) / kLeavesPerBlock, sh->batch), 256, 0,
+             st>>>(c, plan->d_leaves, plan->nleaves, nvals, vals);
+    else
+      colsum_leaf64_kernel<T><<<dim3(plan->nleaves, sh->batch), 512, 0, st>>>(c, plan->d_leaves,
+                                                                              nvals, vals);
   } else {
     dim3 lgrid(plan->nleaves, (K + 31) / 32, sh->batch);
     colsum_leaf_kernel<T><<<lgrid, dim3(32, 8), 0, st>>>(c, plan->d_leaves, nvals, vals);
@@ -670,11 +755,11 @@ static int colsum_t(const s2v_shard *sh, int K, const void *h, void *g, void *wo
   S2V_LAUNCH_CHECK();
   const int nlv = (int)plan->level_start.size() - 1;
   int lv = 0;
-  // wide heights: one launch each; the rest (<= 512 nodes per height): one CTA
+  // wide heights: one launch each; the rest (<= 64 nodes per height): one CTA
   for (; lv < nlv; lv++) {
     const int a = plan->level_start[lv], bnd = plan->level_start[lv + 1];
     const int count = bnd - a;
-    if (count <= 512) break;
+    if (count <= 64) break;
     int64_t work = (int64_t)count * K;
     int blocks = (int)std::min<int64_t>((work + 255) / 256, kNumSMs * 8);
     colsum_level_kernel<T><<<dim3(blocks, sh->batch), 256, 0, st>>>(
@@ -758,9 +843,10 @@ __global__ void __launch_bounds__(256) score_generic_kernel(
 #pragma unroll
   for (int q = 0; q < kTopK; q++) top[q] = null_key();
   unsigned long long cnt = 0;
-  const int64_t i0 = (int64_t)blockIdx.x * kScoreRowsPerBlock;
-  const int64_t i1 = min(i0 + kScoreRowsPerBlock, sh.num_rows);
-  for (int64_t i = i0 + warp; i < i1; i += 8) {
+  // rows dealt to blocks in chunks of kScoreRowsPerBlock, round-robin
+  for (int64_t c0 = (int64_t)blockIdx.x * kScoreRowsPerBlock; c0 < sh.num_rows;
+       c0 += (int64_t)gridDim.x * kScoreRowsPerBlock)
+  for (int64_t i = c0 + warp, c1 = min(c0 + kScoreRowsPerBlock, sh.num_rows); i < c1; i += 8) {
     const int64_t r = (int64_t)b * sh.num_rows + i;
     const bool c = (cand_override ? cand_override[r] : sh.cand[r]) != 0;
     const int64_t phys = ((int64_t)b * sh.world + sh.rank) * sh.rows_max + i;
@@ -811,8 +897,11 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
   __shared__ unsigned long long s_count;
   Key *s_keys = reinterpret_cast<Key *>(xbuf);
   const int b = blockIdx.y, tid = threadIdx.x;
-  if (sh.active && (int64_t)blockIdx.x * kScoreRowsPerBlock >= sh.active_n[0]) {
-    // past the end of the active list: no rows, no keys
+  // 64-row tiles are dealt to blocks round-robin (tile t -> block t mod
+  // gridDim.x), so a short active list still spreads over every block
+  const int64_t lim = sh.active ? sh.active_n[0] : sh.num_rows;
+  if ((int64_t)blockIdx.x * kScoreTile >= lim) {
+    // no tile for this block: no rows, no keys
     if (tid < kTopK) block_keys[((int64_t)b * gridDim.x + blockIdx.x) * kTopK + tid] = null_key();
     return;
   }
@@ -830,8 +919,9 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
   unsigned long long cnt = 0;
   // positions [i0, i1) of this block: local rows, or entries of the active
   // list (B = 1) when set -- rows off the list have rdeg = 0, not candidates
-  const int64_t i0 = (int64_t)blockIdx.x * kScoreRowsPerBlock;
-  const int64_t i1 = min(i0 + kScoreRowsPerBlock, sh.active ? sh.active_n[0] : sh.num_rows);
+  const int64_t i0 = (int64_t)blockIdx.x * kScoreTile;
+  const int64_t tstride = (int64_t)gridDim.x * kScoreTile;
+  const int64_t i1 = lim;
   const int64_t base_r = (int64_t)b * sh.num_rows;
   const int64_t base_phys = ((int64_t)b * sh.world + sh.rank) * sh.rows_max;
   const int kq = tid & 15, rq = tid >> 4;
@@ -858,7 +948,7 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
     }
   };
   load_tile(i0);
-  for (int64_t t0 = i0; t0 < i1; t0 += kScoreTile) {
+  for (int64_t t0 = i0; t0 < i1; t0 += tstride) {
     __syncthreads();
     // x = h * cand (fl(h*1) = h, fl(h*0) = +-0)
 #pragma unroll
@@ -879,7 +969,7 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
       xT[(k4 * 4 + 3) * 64 + rsw] = __fmul_rn(pre[q].w, c);
     }
     __syncthreads();
-    load_tile(t0 + kScoreTile);
+    load_tile(t0 + tstride);
     float acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; a++)
@@ -951,9 +1041,8 @@ __global__ void topk_below_kernel(s2v_shard sh, const Key *__restrict__ keys,
   Key top[kTopK];
 #pragma unroll
   for (int q = 0; q < kTopK; q++) top[q] = null_key();
-  const int64_t i0 = (int64_t)blockIdx.x * kScoreRowsPerBlock;
-  const int64_t i1 = min(i0 + kScoreRowsPerBlock, sh.num_rows);
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sh.num_rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
     const Key k = keys[(int64_t)b * sh.num_rows + i];
     if (key_gt(ceil, k)) insert_top(top, k);
   }
@@ -973,7 +1062,7 @@ __global__ void topk_merge_kernel(const Key *__restrict__ block_keys, int nblk, 
   // active-row list: only its first blocks hold keys (the rest are empty)
   int used = nblk;
   if (active_n) {
-    const int64_t act_blk = (active_n[0] + kScoreRowsPerBlock - 1) / kScoreRowsPerBlock;
+    const int64_t act_blk = (active_n[0] + kScoreTile - 1) / kScoreTile;  // blocks with a tile
     if (act_blk < used) used = (int)act_blk;
   }
   const int64_t total = (int64_t)used * kTopK;
@@ -1178,7 +1267,9 @@ int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
 }
 
 int s2v_score_blocks(const s2v_shard *sh) {
+  // one resident wave (3 CTAs per SM) at most; rows are dealt round-robin
   int64_t n = (sh->num_rows + kScoreRowsPerBlock - 1) / kScoreRowsPerBlock;
+  if (n > kNumSMs * 3) n = kNumSMs * 3;
   return (int)(n < 1 ? 1 : n);
 }
 
