@@ -58,9 +58,18 @@ __device__ __forceinline__ int64_t phys_of(const s2v_shard &sh, const PartitionM
 __global__ void shard_init_kernel(s2v_shard sh, const uint8_t *__restrict__ sol_phys) {
   const int lane = threadIdx.x & 31;
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  // per-warp running count of alive entries, flushed once per slot (one
+  // atomic per warp and slot instead of one per row)
+  int64_t acc_b = -1;
+  unsigned long long acc = 0;
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < nrows;
        r += (gridDim.x * (int64_t)blockDim.x) >> 5) {
     const int64_t b = r / sh.num_rows, i = r - b * sh.num_rows;
+    if (b != acc_b) {
+      if (lane == 0 && acc) atomicAdd((unsigned long long *)&sh.residual[acc_b], acc);
+      acc_b = b;
+      acc = 0;
+    }
     const uint8_t s = sol_phys[(b * sh.world + sh.rank) * sh.rows_max + i];
     int cnt = 0;
     for (int64_t e = sh.row_ptr[r] + lane; e < sh.row_ptr[r + 1]; e += 32) {
@@ -75,9 +84,10 @@ __global__ void shard_init_kernel(s2v_shard sh, const uint8_t *__restrict__ sol_
       sh.rdeg[r] = cnt;
       sh.sol[r] = s;
       sh.cand[r] = (cnt > 0 && !s) ? 1 : 0;
-      if (cnt) atomicAdd((unsigned long long *)&sh.residual[b], (unsigned long long)cnt);
+      acc += (unsigned long long)cnt;
     }
   }
+  if (lane == 0 && acc) atomicAdd((unsigned long long *)&sh.residual[acc_b], acc);
 }
 
 // Is the edge (row r, neighbour phys q) present and alive?  Row cols are

@@ -16,7 +16,9 @@ dumps = sorted(int(x) for x in sys.argv[4].split(",")) if len(sys.argv) > 4 else
 g = P.generate_rmat(scale, 16, 0) if kind == "rmat" else P.generate_ba(scale, 16, 0)
 comm = P.WorkerGroup(1).comm(0)
 params = P.PolicyParams.initialize(64, 5, seed=0)
-st = P.PartitionedState([g], P.partition_rows(g.num_nodes, 1)[0])
+start = os.environ.get("S2V_START_SOL")  # resume from a saved partial solution
+sol = None if not start else np.unpackbits(np.load(start))[:g.num_nodes][None]
+st = P.PartitionedState([g], P.partition_rows(g.num_nodes, 1)[0], solutions=sol)
 ep = DeviceEpisode(st, params, comm, P.SelectionSchedule.adaptive(), 1, use_graph=False)
 tail_rows = int(os.environ.get("S2V_TAIL_ROWS", "65536"))
 tail = False
@@ -34,7 +36,7 @@ while active.any():
         np.save(f"gpurun_out/sol_{kind}{scale}_{dumps.pop(0)}.npy",
                 np.packbits(st.sol_d.to("cpu").numpy()[:g.num_nodes]))
     now = time.perf_counter() - t0
-    if now - last_t > 5 or not active.any() or now > budget:
+    if now - last_t > 5 or not active.any() or now > budget or os.environ.get("S2V_VERBOSE"):
         d = int((tp[-1, 0] >= 0).sum())
         print(f"t {now:7.1f}s evals {evals:7d} active {ep.active_count():8d} alive "
               f"{int(st.residual_d.sum().item()):10d} d {d} "
