@@ -173,6 +173,21 @@ int s2v_active_compact(const s2v_shard *sh, int32_t *list, int64_t *n, int32_t *
                        void *stream);
 int64_t s2v_active_workspace(int64_t cap);
 
+/* Incremental-forward frontier (B = 1, P = 1; csrc/s2v_frontier.cu): the
+ * rows whose round-l embedding may change after a group apply -- the picks
+ * and their alive neighbours (seed, called BEFORE s2v_apply_phase2), then
+ * `levels`-1 hops over the residual graph (expand, AFTER the apply).  D
+ * [rows] gets the rows in BFS order, meta [s2v_frontier_meta_size(levels)]
+ * the level prefixes: {meta[4+2l], 0} is the active_n pair of round l.
+ * mark [rows] int32 stamps (zero-initialised once).  A frontier larger than
+ * cap is replaced by the active list act[0, act_n[0]) for every level. */
+int s2v_frontier_seed(const s2v_shard *sh, const int64_t *picks, int d, int levels, int32_t *D,
+                      int64_t *meta, int32_t *mark, int64_t cap, void *stream);
+int s2v_frontier_expand(const s2v_shard *sh, int levels, int32_t *D, int64_t *meta, int32_t *mark,
+                        int64_t cap, const int32_t *act, const int64_t *act_n, int64_t act_cap,
+                        void *stream);
+int64_t s2v_frontier_meta_size(int levels);
+
 /* g[b][k] = numpy pairwise sum over the N nodes of slot b of h[.,k]; h must
  * hold every rank's rows (after an all-gather when P>1).  Replaces
  * embed.sum(axis=2) + q_fwd all-reduce (policy.py:199-200). */
@@ -190,7 +205,12 @@ size_t s2v_colsum_workspace(const s2v_shard *sh, int K, int elem_bytes);
  * (first call). */
 int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
                         const void *h1_table, int max_deg, void *g, void *workspace,
-                        size_t workspace_bytes, uint8_t *last, int full, void *stream);
+                        size_t workspace_bytes, uint8_t *last, int full,
+                        const int32_t *dirty_rows, const int64_t *ndirty, void *stream);
+/* (dirty_rows, ndirty: incremental forward -- only the leaves holding one of
+ * these rows (every row whose embedding changed) are recomputed.)  Workspace
+ * bytes for s2v_colsum_residual: */
+size_t s2v_colsum_residual_workspace(const s2v_shard *sh, int K, int elem_bytes);
 
 /* Scores of this rank's rows: u2 = theta6 (h*cand), r = relu([u1;u2]),
  * score = sum_j fl(r_j theta7_j) (policy.py:201-207), masked selection keys
@@ -204,6 +224,17 @@ int s2v_score(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, const voi
               const void *theta6, const void *theta7, const uint8_t *cand_override,
               int mode, void *scores, uint64_t *block_keys, int64_t *counts, void *stream);
 int s2v_score_blocks(const s2v_shard *sh);
+/* Scores of an active-row list (B = 1, P = 1, K = 64 fp32) with a per-row
+ * cache of the theta7 terms fl(relu(u2_k) theta7_{K+k}), prod_cache[rows][64]:
+ * rows == NULL scores every list row and fills the cache; otherwise the
+ * cache is refreshed for rows[0, nrows[0]) (the incremental frontier) and
+ * every candidate's score is s0 + its cached terms, summed in the same
+ * order (policy.py:201-207).  Keys and counts as s2v_score; scores[] is
+ * written only by the rows == NULL form. */
+int s2v_score_cached(const s2v_shard *sh, const float *h, const float *u1, const float *theta6,
+                     const float *theta7, int mode, float *prod_cache, const int32_t *rows,
+                     const int64_t *nrows, float *scores, uint64_t *block_keys, int64_t *counts,
+                     void *stream);
 /* Merge per-block keys into the top-d (d <= 8) keys per slot, descending.
  * A key is two uint64 {orderable(score), ~node}; {0,0} = none. */
 int s2v_topk_merge(const s2v_shard *sh, const uint64_t *block_keys, int d, uint64_t *top,

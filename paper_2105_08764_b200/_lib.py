@@ -71,7 +71,12 @@ _SIGNATURES = {
     "s2v_embed_round_peers": ([_I, _SH, _P, _P, _I, _I, _P, _P, _P, _I, _P, _P], _I),
     "s2v_colsum": ([_I, _SH, _I, _P, _P, _P, _SZ, _P], _I),
     "s2v_colsum_workspace": ([_SH, _I, _I], _SZ),
-    "s2v_colsum_residual": ([_I, _SH, _I, _P, _P, _I, _P, _P, _SZ, _P, _I, _P], _I),
+    "s2v_colsum_residual": ([_I, _SH, _I, _P, _P, _I, _P, _P, _SZ, _P, _I, _P, _P, _P], _I),
+    "s2v_colsum_residual_workspace": ([_SH, _I, _I], _SZ),
+    "s2v_score_cached": ([_SH, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P], _I),
+    "s2v_frontier_seed": ([_SH, _P, _I, _I, _P, _P, _P, _I64, _P], _I),
+    "s2v_frontier_expand": ([_SH, _I, _P, _P, _P, _I64, _P, _P, _I64, _P], _I),
+    "s2v_frontier_meta_size": ([_I], _I64),
     "s2v_active_compact": ([_SH, _P, _P, _P, _P, _I64, _P, _P, _P], _I),
     "s2v_active_workspace": ([_I64], _I64),
     "s2v_score": ([_I, _SH, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P], _I),

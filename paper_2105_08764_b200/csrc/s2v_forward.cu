@@ -375,6 +375,9 @@ struct PairwiseCtx {
   // call (0 live, 1/2 dead); a leaf dead now and then keeps its value
   uint8_t *last;
   int full;
+  // incremental forward: only leaves flagged here (rows whose value changed)
+  // are recomputed, the rest keep their cached sums
+  const uint8_t *leaf_dirty;
 };
 
 __device__ __forceinline__ int64_t phys_node(const PairwiseCtx &c, int64_t u) {
@@ -468,8 +471,10 @@ __global__ void __launch_bounds__(512) colsum_leaf64_kernel(PairwiseCtx c,
       }
     }
     if (tid < 128) s_dead[tid >> 6][k] = reinterpret_cast<const T *>(c.dead)[tid];
-    // every row dead now and at the previous call: the cached value stands
-    if (!__syncthreads_or(live || c.full || !c.last)) return;
+    // every row dead now and at the previous call (or, with leaf flags, no
+    // row changed): the cached value stands
+    const bool redo = c.leaf_dirty ? (c.full || c.leaf_dirty[leaf]) : (live || c.full || !c.last);
+    if (!__syncthreads_or(redo)) return;
   }
   // generic pointer to row i's value: a dead row's lives in shared memory
   auto src = [&](int64_t i) -> const T * {
@@ -532,7 +537,11 @@ __global__ void __launch_bounds__(256) colsum_leaf64x4_kernel(PairwiseCtx c,
   const T *h = reinterpret_cast<const T *>(c.h);
   const bool res = c.dead != nullptr;
   if (res) {
-    if (tid < kLeavesPerBlock) s_live[tid] = (c.full || !c.last) ? 1 : 0;
+    if (tid < kLeavesPerBlock) {
+      const int lf = blockIdx.x * kLeavesPerBlock + tid;
+      s_live[tid] = (c.full || !c.last) ? 1
+                    : (c.leaf_dirty && lf < nleaves && c.leaf_dirty[lf]) ? 1 : 0;
+    }
     if (tid < 128) s_dead[tid >> 6][k] = reinterpret_cast<const T *>(c.dead)[tid];
     __syncthreads();
     bool live = false;
@@ -550,9 +559,9 @@ __global__ void __launch_bounds__(256) colsum_leaf64x4_kernel(PairwiseCtx c,
         }
       }
     }
-    if (live) s_live[ll] = 1;
+    if (live && !c.leaf_dirty) s_live[ll] = 1;
     __syncthreads();
-    if (!s_live[ll]) return;  // all dead now and at the previous call
+    if (!s_live[ll]) return;  // all dead now and at the previous call / unchanged
   }
   if (!ok) return;
   auto src = [&](int64_t i) -> const T * {
@@ -710,10 +719,31 @@ static int get_plan(int64_t N, PairwisePlan **out) {
   return S2V_OK;
 }
 
+// flags[leaf of u] = 1 for every row u of the list (leaf starts ascending)
+__global__ void mark_leaves_kernel(const int64_t *__restrict__ leaves, int nleaves,
+                                   const int32_t *__restrict__ rows,
+                                   const int64_t *__restrict__ nrows, uint8_t *__restrict__ flags) {
+  const int64_t n = nrows[0];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = rows[j];
+    int lo = 0, hi = nleaves - 1;  // last leaf with start <= u
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (leaves[2 * mid] <= u)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    flags[lo] = 1;
+  }
+}
+
 template <class T>
 static int colsum_t(const s2v_shard *sh, int K, const void *h, void *g, void *workspace,
                     size_t workspace_bytes, cudaStream_t st, const T *dead = nullptr,
-                    uint8_t *last = nullptr, int full = 1) {
+                    uint8_t *last = nullptr, int full = 1, const int32_t *dirty_rows = nullptr,
+                    const int64_t *ndirty = nullptr, uint8_t *flags = nullptr) {
   PairwisePlan *plan = nullptr;
   int rc = get_plan(sh->num_nodes, &plan);
   if (rc) return rc;
@@ -735,7 +765,16 @@ static int colsum_t(const s2v_shard *sh, int K, const void *h, void *g, void *wo
   c.sol = sh->sol;
   c.last = last;
   c.full = full;
+  c.leaf_dirty = nullptr;
   if (last && K != 64) return fail(S2V_EINVAL, "incremental colsum needs K = 64");
+  if (dirty_rows) {
+    if (!last || !flags || sh->batch != 1) return fail(S2V_EINVAL, "bad dirty-row colsum args");
+    S2V_CUDA_CHECK(cudaMemsetAsync(flags, 0, plan->nleaves, st));
+    mark_leaves_kernel<<<kNumSMs * 2, 256, 0, st>>>(plan->d_leaves, plan->nleaves, dirty_rows,
+                                                    ndirty, flags);
+    S2V_LAUNCH_CHECK();
+    c.leaf_dirty = flags;
+  }
   if (K == 64) {
     static const bool x4 = [] {
       const char *e = getenv("S2V_COLSUM_X4");
@@ -883,7 +922,10 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
     s2v_shard sh, const float *__restrict__ h, const float *__restrict__ u1,
     const float *__restrict__ theta6, const float *__restrict__ theta7,
     const uint8_t *__restrict__ cand_override, int mode, float *__restrict__ scores,
-    Key *__restrict__ block_keys, int64_t *__restrict__ counts) {
+    Key *__restrict__ block_keys, int64_t *__restrict__ counts,
+    float *__restrict__ prod_cache = nullptr, int emit = 1) {
+  // prod_cache (nullable, [rows][64]): keep each row's fl(relu(u2) * theta7)
+  // terms for score_sum64_kernel; emit = 0: only fill the cache
   __shared__ __align__(16) float th6T[64][68];           // th6T[p][k] = theta6[k][p]
   // xT[p][row] = h[row][p]*c; after the projection the same storage holds
   // prod[row][k] = fl(relu(u2) * theta7), and at the end the key lists
@@ -996,8 +1038,18 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
 #pragma unroll
       for (int c = 0; c < 4; c++)
         prod[rq * 4 + a][kq * 4 + c] = __fmul_rn(relu(acc[a][c]), s_t7[kq * 4 + c]);
+    if (prod_cache) {
+#pragma unroll
+      for (int a = 0; a < 4; a++) {
+        const int32_t i = s_i[rq * 4 + a];
+        if (i >= 0)
+          *reinterpret_cast<float4 *>(prod_cache + (int64_t)i * 64 + kq * 4) =
+              make_float4(prod[rq * 4 + a][kq * 4 + 0], prod[rq * 4 + a][kq * 4 + 1],
+                          prod[rq * 4 + a][kq * 4 + 2], prod[rq * 4 + a][kq * 4 + 3]);
+      }
+    }
     __syncthreads();
-    if (tid < kScoreTile && t0 + tid < i1) {
+    if (emit && tid < kScoreTile && t0 + tid < i1) {
       float sc = s_s0;
 #pragma unroll 16
       for (int k = 0; k < 64; k++) sc = __fadd_rn(sc, prod[tid][k]);
@@ -1014,6 +1066,58 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
   block_merge_top(top, s_keys, block_keys + ((int64_t)b * gridDim.x + blockIdx.x) * kTopK,
                   kScoreTile);
   if (tid == 0 && s_count) atomicAdd((unsigned long long *)&counts[b], s_count);
+}
+
+// Scores of the active list from cached theta7 terms (incremental forward):
+// score = s0 + sum_k prod_cache[row][k], the same sequential adds as
+// score64_kernel, with s0 from this evaluation's u1.  A candidate's cached
+// terms are current: its h_L is unchanged unless it was in the frontier,
+// whose rows were refreshed by score64_kernel(emit = 0) first.  One thread
+// per row, rows dealt round-robin; per-block top-8 keys and counts as
+// score64_kernel (scores are not written).
+__global__ void __launch_bounds__(256) score_sum64_kernel(s2v_shard sh,
+                                                          const float *__restrict__ u1,
+                                                          const float *__restrict__ theta7,
+                                                          const float *__restrict__ prod_cache,
+                                                          int mode, Key *__restrict__ block_keys,
+                                                          int64_t *__restrict__ counts) {
+  __shared__ Key s_keys[256 * kTopK];
+  __shared__ float s_s0;
+  __shared__ unsigned long long s_count;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    float s0 = 0.f;
+    for (int j = 0; j < 64; j++) s0 = __fadd_rn(s0, __fmul_rn(relu(u1[j]), theta7[j]));
+    s_s0 = s0;
+    s_count = 0;
+  }
+  __syncthreads();
+  Key top[kTopK];
+#pragma unroll
+  for (int q = 0; q < kTopK; q++) top[q] = null_key();
+  unsigned long long cnt = 0;
+  const int64_t n = sh.active_n[0];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + tid; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = sh.active[j];
+    if (!sh.cand[i]) continue;
+    const float4 *pc = reinterpret_cast<const float4 *>(prod_cache + (int64_t)i * 64);
+    float sc = s_s0;
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const float4 v = pc[q];
+      sc = __fadd_rn(sc, v.x);
+      sc = __fadd_rn(sc, v.y);
+      sc = __fadd_rn(sc, v.z);
+      sc = __fadd_rn(sc, v.w);
+    }
+    const bool finite = isfinite(sc);
+    if (finite) cnt++;
+    if (finite || mode == 1) insert_top(top, make_key((double)sc, sh.row_start + i));
+  }
+  if (cnt) atomicAdd(&s_count, cnt);
+  block_merge_top(top, s_keys, block_keys + (int64_t)blockIdx.x * kTopK);
+  if (tid == 0 && s_count) atomicAdd((unsigned long long *)&counts[0], s_count);
 }
 
 // Per-row selection keys from the scores (mode 0: candidates with a finite
@@ -1244,26 +1348,36 @@ int s2v_colsum(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, void *g,
   return colsum_t<double>(sh, K, h, g, workspace, workspace_bytes, as_stream(stream));
 }
 
+size_t s2v_colsum_residual_workspace(const s2v_shard *sh, int K, int elem_bytes) {
+  // tree values, the two dead-row embeddings, one flag byte per leaf
+  return s2v_colsum_workspace(sh, K, elem_bytes) + 2 * (size_t)K * elem_bytes +
+         (size_t)(sh->num_nodes / 56 + 2) + 16;
+}
+
 int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
                         const void *h1_table, int max_deg, void *g, void *workspace,
-                        size_t workspace_bytes, uint8_t *last, int full, void *stream) {
+                        size_t workspace_bytes, uint8_t *last, int full,
+                        const int32_t *dirty_rows, const int64_t *ndirty, void *stream) {
   if (sh->world != 1) return fail(S2V_EINVAL, "residual colsum needs P = 1");
   if (max_deg < 0 || !h1_table) return fail(S2V_EINVAL, "bad residual colsum args");
   cudaStream_t st = as_stream(stream);
   const size_t elem = dt == S2V_F32 ? 4 : 8;
   const size_t need = s2v_colsum_workspace(sh, K, (int)elem);
-  if (workspace_bytes < need + 2 * K * elem)
+  if (workspace_bytes < s2v_colsum_residual_workspace(sh, K, (int)elem))
     return fail(S2V_EINVAL, "residual colsum workspace too small");
   void *dead = (char *)workspace + need;  // after the tree values
+  uint8_t *flags = (uint8_t *)dead + 2 * K * elem;
   if (dt == S2V_F32) {
     dead_rows_kernel<float><<<1, 64, 0, st>>>((const float *)h1_table, K, max_deg, (float *)dead);
     S2V_LAUNCH_CHECK();
-    return colsum_t<float>(sh, K, h, g, workspace, need, st, (const float *)dead, last, full);
+    return colsum_t<float>(sh, K, h, g, workspace, need, st, (const float *)dead, last, full,
+                           dirty_rows, ndirty, flags);
   }
   dead_rows_kernel<double><<<1, 64, 0, st>>>((const double *)h1_table, K, max_deg,
                                              (double *)dead);
   S2V_LAUNCH_CHECK();
-  return colsum_t<double>(sh, K, h, g, workspace, need, st, (const double *)dead, last, full);
+  return colsum_t<double>(sh, K, h, g, workspace, need, st, (const double *)dead, last, full,
+                          dirty_rows, ndirty, flags);
 }
 
 int s2v_score_blocks(const s2v_shard *sh) {
@@ -1305,6 +1419,35 @@ int s2v_score(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, const voi
                                   cand_override, mode, (double *)scores, (Key *)block_keys,
                                   counts);
   }
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_score_cached(const s2v_shard *sh, const float *h, const float *u1, const float *theta6,
+                     const float *theta7, int mode, float *prod_cache, const int32_t *rows,
+                     const int64_t *nrows, float *scores, uint64_t *block_keys, int64_t *counts,
+                     void *stream) {
+  if (!sh->active || sh->batch != 1 || sh->world != 1 || !prod_cache)
+    return fail(S2V_EINVAL, "cached scores need an active-row list, B = 1, P = 1");
+  cudaStream_t st = as_stream(stream);
+  S2V_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(int64_t), st));
+  const int nblk = s2v_score_blocks(sh);
+  if (!rows) {  // every active row: scores, keys, and the cache
+    score64_kernel<<<dim3(nblk, 1), 256, 0, st>>>(*sh, h, u1, theta6, theta7, nullptr, mode,
+                                                  scores, (Key *)block_keys, counts, prod_cache, 1);
+    S2V_LAUNCH_CHECK();
+    return S2V_OK;
+  }
+  s2v_shard fr = *sh;  // refresh the cached terms of the frontier rows
+  fr.active = rows;
+  fr.active_n = nrows;
+  fr.active_ptr = nullptr;
+  fr.active_cols = nullptr;
+  score64_kernel<<<dim3(nblk, 1), 256, 0, st>>>(fr, h, u1, theta6, theta7, nullptr, mode, scores,
+                                                (Key *)block_keys, counts, prod_cache, 0);
+  S2V_LAUNCH_CHECK();
+  score_sum64_kernel<<<nblk, 256, 0, st>>>(*sh, u1, theta7, prod_cache, mode, (Key *)block_keys,
+                                           counts);
   S2V_LAUNCH_CHECK();
   return S2V_OK;
 }

@@ -59,9 +59,14 @@ def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
 
-def to_device(arr: np.ndarray, device=None) -> torch.Tensor:
+def to_device(arr: np.ndarray, device=None, pinned: bool = False) -> torch.Tensor:
+    """Host array -> new device tensor.  pinned: stage through page-locked
+    memory and copy asynchronously on the current stream (ordered before any
+    later kernel on that stream)."""
     arr = np.ascontiguousarray(arr)
     t = torch.from_numpy(arr)
+    if pinned:
+        return t.pin_memory().to(device or current_device(), non_blocking=True)
     return t.to(device or current_device(), non_blocking=False)
 
 

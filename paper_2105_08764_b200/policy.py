@@ -219,7 +219,10 @@ def _buffers(state: PartitionedState, k: int, dtype, count: int):
     tdt = _torch_dtype(dtype)
 
     def make():
-        return [torch.zeros(n_el, dtype=tdt, device=state.device) for _ in range(count)]
+        # P = 1: every round writes every row before anything reads it (no
+        # padding rows), so no zero-fill pass over the buffers is needed
+        alloc = torch.empty if state.world == 1 else torch.zeros
+        return [alloc(n_el, dtype=tdt, device=state.device) for _ in range(count)]
     return state.workspace(f"h{count}", (k, np.dtype(dtype).str, count), make)
 
 
@@ -260,12 +263,16 @@ def _degree_table_round2(state: PartitionedState, k: int, dt: int, num_layers: i
 
 
 def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers: int, comm,
-                    dtype, tape: bool, reuse_tables: bool = False):
+                    dtype, tape: bool, reuse_tables: bool = False, persist: bool = False,
+                    round_rows=None):
     """L embedding rounds.  Returns the list of h buffers (all of them when
     tape, else the final one) and, when tape, the m buffers per round.
     reuse_tables: the e12 / h1 tables of this state were last built from
     these same device parameters (an episode's later evaluations) -- skip
-    rebuilding them."""
+    rebuilding them.  persist: one buffer per layer (not ping-pong), so that
+    every layer's rows survive to the next evaluation (incremental forward).
+    round_rows(layer) -> (row list, active_n pair) device pointers: round
+    layer+1 visits only those rows (the incremental frontier, full CSR)."""
     k = dparams.k
     dt = _dt_code(dtype)
     st = stream_ptr()
@@ -276,15 +283,16 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
     if not reuse:
         _lib.call("s2v_e12_table", dt, dparams.ptr("theta1"), dparams.ptr("theta2"),
                   dparams.ptr("theta3"), k, max_deg, ptr(table), st)
-    if tape:
+    if tape or persist:
         hs = _buffers(state, k, dtype, num_layers)
+    else:
+        hs = _buffers(state, k, dtype, 2)
+    ms = None
+    if tape:
         rows = state.batch * state.part.num_rows
         ms = state.workspace("mtape", (k, np.dtype(dtype).str, num_layers), lambda: [
             torch.empty(max(rows * k, 1), dtype=_torch_dtype(dtype), device=state.device)
             for _ in range(num_layers)])
-    else:
-        hs = _buffers(state, k, dtype, 2)
-        ms = None
     h_prev = None
     out = []
     h1t = None
@@ -297,9 +305,14 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
     elif state.active_on:
         raise RuntimeError("active-row lists need the degree-table round (K = 64 fp32, P = 1)")
     state._tables_of = dparams
+    sh = state.shard
+    outer = (sh.active, sh.active_n, sh.active_ptr, sh.active_cols)
     for layer in range(num_layers):
-        h_out = hs[layer] if tape else hs[layer % 2]
+        h_out = hs[layer] if (tape or persist) else hs[layer % 2]
         m_out = ms[layer] if (tape and layer > 0) else None
+        if round_rows is not None and layer > 0:
+            rows_ptr, n_ptr = round_rows(layer)
+            sh.active, sh.active_n, sh.active_ptr, sh.active_cols = rows_ptr, n_ptr, None, None
         if h1t is not None and layer == 0 and not tape:
             # inference: nothing reads h1 but round 2, which reads the table
             out.append(None)
@@ -307,6 +320,7 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
         if h1t is not None and layer == 1:
             _lib.call("s2v_embed_round2_table", dt, state.shard_ref(), dparams.ptr("theta4"),
                       ptr(table), k, max_deg, ptr(h1t), ptr(h_out), ptr(m_out), st)
+            sh.active, sh.active_n, sh.active_ptr, sh.active_cols = outer
             h_prev = h_out
             out.append(h_out)
             continue
@@ -330,6 +344,7 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
                       ptr(table), k, max_deg, ptr(h_prev), ptr(h_out), ptr(m_out), st)
             _allgather_rows(state, comm, h_out, k, "embed_fwd",
                             name=f"h{layer if tape else layer % 2}/{len(hs)}")
+        sh.active, sh.active_n, sh.active_ptr, sh.active_cols = outer
         if timer is not None:
             ev1.record()
             timer.append((ev0, ev1))
@@ -359,8 +374,9 @@ def _colsum_device(emb: DeviceEmbedding) -> torch.Tensor:
     left on the device ([B][K])."""
     st = emb.state
     k = emb.k
-    wsb = _lib.load().s2v_colsum_workspace(st.shard_ref(), k, emb.dtype.itemsize)
-    wsb += 2 * k * emb.dtype.itemsize  # the two dead-row embeddings (residual mode)
+    lib = _lib.load()
+    wsb = max(lib.s2v_colsum_workspace(st.shard_ref(), k, emb.dtype.itemsize),
+              lib.s2v_colsum_residual_workspace(st.shard_ref(), k, emb.dtype.itemsize))
     ws = st.workspace("colsum", (k, emb.dtype.str), lambda: {
         "ws": torch.empty(max(wsb // emb.dtype.itemsize, 1), dtype=_torch_dtype(emb.dtype),
                           device=st.device),
@@ -374,15 +390,18 @@ def _colsum_device(emb: DeviceEmbedding) -> torch.Tensor:
         if inc is None:
             _lib.call("s2v_colsum_residual", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h),
                       ptr(h1t), int(st.max_deg), ptr(ws["g"]), ptr(ws["ws"]), wsb, None, 1,
-                      stream_ptr())
+                      None, None, stream_ptr())
         else:
             if inc.get("ws") is None:
                 inc["ws"] = torch.empty_like(ws["ws"])
                 inc["last"] = torch.zeros(st.batch * st.num_nodes, dtype=torch.uint8,
                                           device=st.device)
+            # incremental forward: (rows, count) whose embedding changed
+            dirty = inc.get("dirty") or (None, None)
             _lib.call("s2v_colsum_residual", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h),
                       ptr(h1t), int(st.max_deg), ptr(ws["g"]), ptr(inc["ws"]), wsb,
-                      ptr(inc["last"]), 1 if inc["full"] else 0, stream_ptr())
+                      ptr(inc["last"]), 1 if inc["full"] else 0, dirty[0], dirty[1],
+                      stream_ptr())
             inc["full"] = False
     else:
         _lib.call("s2v_colsum", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h),
@@ -399,6 +418,20 @@ def u1_on_device(batch: int, k: int, dtype) -> bool:
     return np.dtype(dtype) == np.float32 and bool(_lib.load().s2v_u1_exact(batch, k))
 
 
+def score_workspace(st: PartitionedState, k: int, dtype) -> dict:
+    """Device buffers of the scorer: u1, scores, per-block keys, the read-back
+    vector (counts [B] then top keys [B][8][2]) and a candidate override."""
+    dtype = np.dtype(dtype)
+    nblk = _lib.load().s2v_score_blocks(st.shard_ref())
+    rows = st.batch * st.part.num_rows
+    return st.workspace("score", (k, dtype.str), lambda: {
+        "u1": torch.empty(st.batch * k, dtype=_torch_dtype(dtype), device=st.device),
+        "scores": torch.empty(max(rows, 1), dtype=_torch_dtype(dtype), device=st.device),
+        "bkeys": torch.empty(st.batch * nblk * 8 * 2, dtype=torch.int64, device=st.device),
+        "out": torch.empty(st.batch * (1 + 8 * 2), dtype=torch.int64, device=st.device),
+        "cand": torch.empty(max(rows, 1), dtype=torch.uint8, device=st.device)})
+
+
 def _score(emb: DeviceEmbedding, params: PolicyParams, dparams: _DeviceParams,
            cand_override: np.ndarray | None, mode: int, d: int, readback: bool = True):
     """Run the scorer; returns (scores device tensor, top keys (B,d,2) or None,
@@ -410,14 +443,8 @@ def _score(emb: DeviceEmbedding, params: PolicyParams, dparams: _DeviceParams,
         g = _global_sum(emb)
         # policy.py:201 -- the reference's own numpy product, on the host
         u1 = np.ascontiguousarray(g @ params.theta5.T, dtype=params.dtype)
-    nblk = _lib.load().s2v_score_blocks(st.shard_ref())
     rows = st.batch * st.part.num_rows
-    ws = st.workspace("score", (k, emb.dtype.str), lambda: {
-        "u1": torch.empty(st.batch * k, dtype=_torch_dtype(emb.dtype), device=st.device),
-        "scores": torch.empty(max(rows, 1), dtype=_torch_dtype(emb.dtype), device=st.device),
-        "bkeys": torch.empty(st.batch * nblk * 8 * 2, dtype=torch.int64, device=st.device),
-        "out": torch.empty(st.batch * (1 + 8 * 2), dtype=torch.int64, device=st.device),
-        "cand": torch.empty(max(rows, 1), dtype=torch.uint8, device=st.device)})
+    ws = score_workspace(st, k, emb.dtype)
     if device_u1:  # numpy's own accumulation order, reproduced on device
         _lib.call("s2v_u1", _dt_code(emb.dtype), st.batch, k, ptr(_colsum_device(emb)),
                   dparams.ptr("theta5"), ptr(ws["u1"]), stream_ptr())

@@ -207,7 +207,7 @@ class PartitionedState:
         else:
             for r, pr in enumerate(partition_rows(n, P)):
                 sol_phys[:, r, :pr.num_rows] = solutions[:, pr.row_start:pr.row_stop]
-        sol_phys_d = to_device(sol_phys.reshape(-1), dev)
+        sol_phys_d = to_device(sol_phys.reshape(-1), dev, pinned=True)
         _lib.call("s2v_shard_init", ctypes.byref(self._shard), ptr(sol_phys_d), stream_ptr())
         self._host = {}
         self._ws: dict = {}

@@ -26,7 +26,7 @@ t0 = time.perf_counter()
 last_t, last_e, evals = 0.0, 0, 0
 active = np.array([True])
 while active.any():
-    if not tail and ep.active_count() <= tail_rows:
+    if not tail and (ep.active_count() <= tail_rows or ep._mode[2]):
         ep.resize(16, use_graph=True)
         tail = True
         print("tail mode at eval", evals, flush=True)
@@ -40,7 +40,8 @@ while active.any():
         d = int((tp[-1, 0] >= 0).sum())
         print(f"t {now:7.1f}s evals {evals:7d} active {ep.active_count():8d} alive "
               f"{int(st.residual_d.sum().item()):10d} d {d} "
-              f"{(now - last_t) / max(evals - last_e, 1) * 1e3:.3f} ms/eval", flush=True)
+              f"{(now - last_t) / max(evals - last_e, 1) * 1e3:.3f} ms/eval inc {int(ep._mode[2])} "
+              f"overflow {int(ep.front_meta[2].item()) if ep.front is not None else -1}", flush=True)
         last_t, last_e = now, evals
     if now > budget:
         break
