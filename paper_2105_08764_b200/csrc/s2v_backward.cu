@@ -763,7 +763,8 @@ __global__ void __launch_bounds__(256) gather64_kernel(s2v_shard sh,
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (!sh.sol[r])
       acc = gather_row64(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, src, sub, hmask, hbase,
-                         hot_rows, pol_hot, pol_cold);
+                         hot_rows, pol_hot, pol_cold, nullptr, nullptr,
+                         (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
     st4(out + r * 64 + 4 * sub, acc);
   }
 }

@@ -201,9 +201,10 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       const int64_t r = s_rows[lr];
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       if (s_e1[lr] > s_e0[lr])
-        acc = gather_row64<TABLE>(s_e0[lr], s_e1[lr], sh.active_ptr ? sh.active_cols : sh.cols,
-                                  h_in, sub, hmask, hbase, hot_rows, pol_hot, pol_cold, sh.rdeg,
-                                  sh.active_ptr ? sh.sol : nullptr);
+        acc = gather_row64<TABLE>(
+            s_e0[lr], s_e1[lr], sh.active_ptr ? sh.active_cols : sh.cols, h_in, sub, hmask, hbase,
+            hot_rows, pol_hot, pol_cold, sh.rdeg, sh.active_ptr ? sh.sol : nullptr,
+            TABLE ? 0u : (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
       *reinterpret_cast<float4 *>(&ms[lr][sub * 4]) = acc;
       if (m_out && r >= 0) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
     }

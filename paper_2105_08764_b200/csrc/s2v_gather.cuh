@@ -70,7 +70,10 @@ __device__ __forceinline__ float4 gather_row64(int64_t e, const int64_t e1,
                                                unsigned hmask, int hbase, uint32_t hot_rows,
                                                uint64_t pol_hot, uint64_t pol_cold,
                                                const int32_t *__restrict__ deg_of = nullptr,
-                                               const uint8_t *__restrict__ sol_of = nullptr) {
+                                               const uint8_t *__restrict__ sol_of = nullptr,
+                                               uint32_t hot_lo = 0) {
+  // hot rows: [hot_lo, hot_lo + hot_rows) -- the low ids (BA hubs) of the
+  // row's own slot of a block-diagonal batch
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (; e < e1; e += 16) {
     const int cnt = (e1 - e) < 16 ? (int)(e1 - e) : 16;
@@ -89,7 +92,7 @@ __device__ __forceinline__ float4 gather_row64(int64_t e, const int64_t e1,
           v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         } else {
           const float *src = h_in + (int64_t)c[q] * 64 + sub * 4;
-          v[q] = ldg_f4_pol(src, c[q] < hot_rows ? pol_hot : pol_cold);
+          v[q] = ldg_f4_pol(src, c[q] - hot_lo < hot_rows ? pol_hot : pol_cold);
         }
       }
 #pragma unroll
