@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(256) frontier_seed_kernel(s2v_shard sh,
 __global__ void __launch_bounds__(256) frontier_expand_kernel(s2v_shard sh, int level,
                                                               int32_t *__restrict__ D,
                                                               int64_t *__restrict__ meta,
-                                                              int32_t *__restrict__ mark) {
+                                                              int32_t *__restrict__ mark,
+                                                              int64_t cap) {
   if (meta[2]) return;  // overflowed: the evaluation recomputes every row
   const int lane = threadIdx.x & 31;
   const int32_t epoch = (int32_t)meta[1];
@@ -129,7 +130,7 @@ int s2v_frontier_expand(const s2v_shard *sh, int levels, int32_t *D, int64_t *me
   if (sh->batch != 1 || sh->world != 1) return fail(S2V_EINVAL, "frontier needs B = 1, P = 1");
   cudaStream_t st = as_stream(stream);
   for (int l = 2; l <= levels; l++) {
-    frontier_expand_kernel<<<kNumSMs * 2, 256, 0, st>>>(*sh, l, D, meta, mark);
+    frontier_expand_kernel<<<kNumSMs * 2, 256, 0, st>>>(*sh, l, D, meta, mark, cap);
     S2V_LAUNCH_CHECK();
     frontier_close_kernel<<<1, 1, 0, st>>>(meta, l, cap);
     S2V_LAUNCH_CHECK();
