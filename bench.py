@@ -76,19 +76,30 @@ class ClockSampler:
         self._t = threading.Thread(target=self._run, daemon=True)
         self.source = "nvml"
 
+    def _nvml_open(self):
+        """NVML handle opened before the timed region (init takes ~0.1 s)."""
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self._nv = (pynvml, h, bits, mx)
+        except Exception:
+            self._nv = None
+
+    def _nvml_sample(self):
+        pynvml, h, bits, mx = self._nv
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.rows.append((float(sm), mx, {n for n, b in bits.items() if r & b}))
+
     def _nvml(self):
-        import pynvml
-        pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-        bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
-                "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
-                "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
-                "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
-        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         while not self._stop.is_set():
-            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            self.rows.append((float(sm), float(mx), {n for n, b in bits.items() if r & b}))
+            self._nvml_sample()
             self._stop.wait(0.01)
 
     def _smi(self):
@@ -111,16 +122,24 @@ class ClockSampler:
 
     def _run(self):
         try:
+            if self._nv is None:
+                raise RuntimeError("no NVML")
             self._nvml()
         except Exception:
             self.source = "nvidia-smi"
             self._smi()
 
     def __enter__(self):
+        self._nvml_open()
         self._t.start()
         return self
 
     def __exit__(self, *exc):
+        if self._nv is not None:  # one sample at the end of the timed region too
+            try:
+                self._nvml_sample()
+            except Exception:
+                pass
         self._stop.set()
         self._t.join(timeout=10)
 

@@ -135,15 +135,21 @@ constexpr int kTileRows = 32;
 
 // h1_table[t][k] = the round-1 output of a row whose e12 row is t: the
 // round kernel's epilogue with m = 0 (FMA chain over zeros, + e12, relu).
+// The chain over m = 0 is the same for every row t, so each block first
+// runs the 64 chains once into shared memory.
 __global__ void h1_table_kernel(const float *__restrict__ theta4,
                                 const float *__restrict__ table, int rows,
                                 float *__restrict__ h1) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)rows * 64) return;
-  const int k = (int)(idx & 63);
-  float z = 0.f;
-  for (int p = 0; p < 64; p++) z = __fmaf_rn(theta4[k * 64 + p], 0.f, z);
-  h1[idx] = relu(__fadd_rn(table[idx], z));
+  __shared__ float z0[64];
+  if (threadIdx.x < 64) {
+    float z = 0.f;
+    for (int p = 0; p < 64; p++) z = __fmaf_rn(theta4[threadIdx.x * 64 + p], 0.f, z);
+    z0[threadIdx.x] = z;
+  }
+  __syncthreads();
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)rows * 64;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    h1[idx] = relu(__fadd_rn(table[idx], z0[idx & 63]));
 }
 
 template <bool TABLE>
@@ -1313,7 +1319,8 @@ int s2v_h1_table(s2v_dtype dt, const void *theta4, const void *table, int K, int
   if (dt != S2V_F32 || K != 64) return fail(S2V_EINVAL, "h1 table needs K = 64 fp32");
   if (max_deg < 0) return fail(S2V_EINVAL, "bad h1 table args");
   const int rows = max_deg + 2;
-  h1_table_kernel<<<(rows * 64 + 255) / 256, 256, 0, as_stream(stream)>>>(
+  h1_table_kernel<<<(int)std::min<int64_t>(((int64_t)rows * 64 + 255) / 256, kNumSMs * 4), 256, 0,
+                    as_stream(stream)>>>(
       (const float *)theta4, (const float *)table, rows, (float *)h1_table);
   S2V_LAUNCH_CHECK();
   return S2V_OK;
