@@ -102,6 +102,20 @@ int s2v_set_device(int device);
  * mask + row sums of PartitionedState.__init__ (state.py:89-111). */
 int s2v_shard_init(const s2v_shard *sh, const uint8_t *sol_phys, void *stream);
 
+/* Block-diagonal batch assembly (PartitionedState over B graphs): for each
+ * segment, dst[dst_off + i] = src[i] + add, i < len, on 4- or 8-byte
+ * integers -- the per-slot CSR, transpose and order arrays shifted by the
+ * slot's entry / row offsets (state.py:89-105 builds the same block-diagonal
+ * matrix with scipy).  segs is a device array. */
+typedef struct {
+  const void *src;
+  int64_t dst_off; /* elements */
+  int64_t len;     /* elements */
+  int64_t add;
+} s2v_segment;
+int s2v_segment_copy(int elem_bytes, const s2v_segment *segs, int nseg, int64_t max_len,
+                     void *dst, void *stream);
+
 /* Apply one group of picks per slot (picks[B*d], -1 padded, global node ids)
  * with the reference's mid-group skip rule.  Replaces the group loop of
  * inference._solve_batch (inference.py:125-146) and apply_action
@@ -307,6 +321,15 @@ int s2v_head_backward(s2v_dtype dt, const s2v_shard *sh, int K, const void *h_L,
 int s2v_adam(s2v_dtype dt, void *params, const void *grads, void *m, void *v, int64_t n,
              double beta1, double omb1, double beta2, double omb2, double eps, double lr,
              double b1c, double b2c, void *stream);
+/* The same update for iteration `it` of a device-resident train_step loop
+ * (agent.py:235-261): gradients are the first n entries of the fp64 pack of
+ * s2v_reduce_partials, rounded to the parameter dtype; bad[it] is set if
+ * any is non-finite, and the update is skipped if any of bad[0..it] is set
+ * (adam_step rejects a non-finite step before touching state,
+ * policy.py:346-349). */
+int s2v_adam_pack(s2v_dtype dt, void *params, const double *pack, void *m, void *v, int64_t n,
+                  double beta1, double omb1, double beta2, double omb2, double eps, double lr,
+                  double b1c, double b2c, int32_t *bad, int it, void *stream);
 
 /* ---- graph ingestion (graphs.py:125-157) --------------------------------- */
 /* Bit-exact generate_ba from numpy's PCG64 state {state_hi, state_lo, inc_hi,

@@ -62,6 +62,7 @@ _SIGNATURES = {
     "s2v_version": ([], ctypes.c_char_p),
     "s2v_set_device": ([_I], _I),
     "s2v_shard_init": ([_SH, _P, _P], _I),
+    "s2v_segment_copy": ([_I, _P, _I, _I64, _P, _P], _I),
     "s2v_apply_phase1": ([_SH, _P, _I, _P, _I, _P, _P], _I),
     "s2v_apply_phase2": ([_SH, _P, _I, _P, _P, _P, _I, _P], _I),
     "s2v_e12_table": ([_I, _P, _P, _P, _I, _I, _P, _P], _I),
@@ -97,6 +98,8 @@ _SIGNATURES = {
     "s2v_reduce_partials": ([_I, _P, _I, _I, _P, _P], _I),
     "s2v_head_backward": ([_I, _SH, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     "s2v_adam": ([_I, _P, _P, _P, _P, _I64, _D, _D, _D, _D, _D, _D, _D, _D, _P], _I),
+    "s2v_adam_pack": ([_I, _P, _P, _P, _P, _I64, _D, _D, _D, _D, _D, _D, _D, _D, _P, _I, _P],
+                      _I),
     "s2v_comm_unique_id": ([_P, _SZ], _I),
     "s2v_comm_init": ([_P, _I, _I, ctypes.POINTER(ctypes.c_void_p)], _I),
     "s2v_comm_destroy": ([_P], _I),

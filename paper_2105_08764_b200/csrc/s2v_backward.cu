@@ -318,6 +318,39 @@ __global__ void adam_kernel(T *__restrict__ p, const T *__restrict__ g, T *__res
   }
 }
 
+// Device-resident tau loop (train_step): gradients straight from the fp64
+// pack of s2v_reduce_partials, rounded to T as the host's astype would, and
+// adam_step's all-or-nothing non-finite rejection (policy.py:346-349):
+// iteration `it` is skipped, with every later one, once any gradient of it
+// or of an earlier iteration is non-finite (bad[0..it]).
+template <class T>
+__global__ void grad_check_kernel(const double *__restrict__ pack, int64_t n, int32_t *bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite((double)(T)pack[i])) *bad = 1;
+}
+
+template <class T>
+__global__ void adam_pack_kernel(T *__restrict__ p, const double *__restrict__ pack,
+                                 T *__restrict__ m, T *__restrict__ v, int64_t n, T b1, T omb1,
+                                 T b2, T omb2, T eps, T lr, T b1c, T b2c,
+                                 const int32_t *__restrict__ bad, int it) {
+  for (int j = 0; j <= it; j++)
+    if (bad[j]) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T gi = (T)pack[i];
+    const T mi = addT(mulT(b1, m[i]), mulT(omb1, gi));
+    const T vi = addT(mulT(b2, v[i]), mulT(mulT(omb2, gi), gi));
+    m[i] = mi;
+    v[i] = vi;
+    const T mh = mi / b1c;
+    const T vh = vi / b2c;
+    const T upd = mulT(lr, mh) / addT(sqrt(vh), eps);
+    p[i] = p[i] - upd;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K = 64 fp32 fast paths (tiles of 64 rows, 4x4 register tiles).
 // ---------------------------------------------------------------------------
@@ -1005,6 +1038,28 @@ int s2v_adam(s2v_dtype dt, void *params, const void *grads, void *m, void *v, in
     adam_kernel<double><<<grid, 256, 0, as_stream(stream)>>>(
         (double *)params, (const double *)grads, (double *)m, (double *)v, n, beta1, omb1,
         beta2, omb2, eps, lr, b1c, b2c);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_adam_pack(s2v_dtype dt, void *params, const double *pack, void *m, void *v, int64_t n,
+                  double beta1, double omb1, double beta2, double omb2, double eps, double lr,
+                  double b1c, double b2c, int32_t *bad, int it, void *stream) {
+  if (n == 0) return S2V_OK;
+  if (it < 0) return fail(S2V_EINVAL, "bad iteration index");
+  cudaStream_t st = as_stream(stream);
+  int grid = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 4);
+  if (dt == S2V_F32) {
+    grad_check_kernel<float><<<grid, 256, 0, st>>>(pack, n, bad + it);
+    adam_pack_kernel<float><<<grid, 256, 0, st>>>(
+        (float *)params, pack, (float *)m, (float *)v, n, (float)beta1, (float)omb1,
+        (float)beta2, (float)omb2, (float)eps, (float)lr, (float)b1c, (float)b2c, bad, it);
+  } else {
+    grad_check_kernel<double><<<grid, 256, 0, st>>>(pack, n, bad + it);
+    adam_pack_kernel<double><<<grid, 256, 0, st>>>((double *)params, pack, (double *)m,
+                                                   (double *)v, n, beta1, omb1, beta2, omb2, eps,
+                                                   lr, b1c, b2c, bad, it);
+  }
   S2V_LAUNCH_CHECK();
   return S2V_OK;
 }

@@ -392,6 +392,21 @@ __global__ void __launch_bounds__(256) active_fill_kernel(s2v_shard sh,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Block-diagonal batch assembly: dst[seg.dst + i] = src[i] + seg.add for
+// every segment (one grid row per segment), for 4- or 8-byte integers.
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void segment_copy_kernel(const s2v_segment *__restrict__ segs, T *__restrict__ dst) {
+  const s2v_segment sg = segs[blockIdx.y];
+  const T *src = reinterpret_cast<const T *>(sg.src);
+  const T add = (T)sg.add;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < sg.len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[sg.dst_off + i] = src[i] + add;
+}
+
 }  // namespace s2v
 
 using namespace s2v;
@@ -469,6 +484,20 @@ int s2v_active_compact(const s2v_shard *sh, int32_t *list, int64_t *n, int32_t *
     active_fill_kernel<<<fgrid, 256, 0, st>>>(*sh, list, n, row_ptr_out, cols_out);
     S2V_LAUNCH_CHECK();
   }
+  return S2V_OK;
+}
+
+int s2v_segment_copy(int elem_bytes, const s2v_segment *segs, int nseg, int64_t max_len,
+                     void *dst, void *stream) {
+  if (nseg <= 0 || max_len <= 0) return S2V_OK;
+  if (elem_bytes != 4 && elem_bytes != 8) return fail(S2V_EINVAL, "segment copy: 4 or 8 bytes");
+  if (nseg > 65535) return fail(S2V_EINVAL, "segment copy: at most 65535 segments");
+  dim3 grid((unsigned)std::min<int64_t>((max_len + 255) / 256, 1024), (unsigned)nseg);
+  if (elem_bytes == 4)
+    segment_copy_kernel<int32_t><<<grid, 256, 0, as_stream(stream)>>>(segs, (int32_t *)dst);
+  else
+    segment_copy_kernel<int64_t><<<grid, 256, 0, as_stream(stream)>>>(segs, (int64_t *)dst);
+  S2V_LAUNCH_CHECK();
   return S2V_OK;
 }
 

@@ -597,13 +597,26 @@ def loss_and_gradients(state: PartitionedState, actions, targets, params: Policy
     if np.any(actions < 0) or np.any(actions >= n):
         raise ValueError("action node index out of range")
     _check_dtype(state, params)
+    pack = _loss_pack(state, actions, targets, params, _DeviceParams(params, state.device), comm)
+    reduced = pack.to("cpu").numpy()
+    grads = unflatten_arrays(reduced[:-1].astype(dtype), k)
+    return float(reduced[-1]) / b, grads
+
+
+def _loss_pack(state: PartitionedState, actions: np.ndarray, targets: np.ndarray,
+               params: PolicyParams, dparams, comm) -> torch.Tensor:
+    """loss_and_gradients on the device: the fp64 pack [grads in parameter
+    order, summed squared error], identical on every rank; dparams holds the
+    parameters the kernels read."""
+    b = state.batch
+    k = params.embed_dim
+    dtype = np.dtype(params.dtype)
     dt = _dt_code(dtype)
     tdt = _torch_dtype(dtype)
     dev = state.device
     s = stream_ptr()
     L = params.num_layers
     lib = _lib.load()
-    dparams = _DeviceParams(params, dev)
     hs, ms, _ = _forward_rounds(state, dparams, L, comm, dtype, tape=True)
     comm.record("q_fwd", b * k)
     rows = state.batch * state.part.num_rows
@@ -664,9 +677,63 @@ def loss_and_gradients(state: PartitionedState, actions, targets, params: Policy
     if dc is not None:
         dc.allreduce(base, pack.numel(), 1, s)
     comm.record("grad", pack.numel())
-    reduced = pack.to("cpu").numpy()
-    grads = unflatten_arrays(reduced[:-1].astype(dtype), k)
-    return float(reduced[-1]) / b, grads
+    return pack
+
+
+def train_iterations(state: PartitionedState, actions, targets, params: PolicyParams,
+                     adam: "AdamState", tau: int, comm) -> list[float]:
+    """tau x (loss_and_gradients + adam_step) of train_step (agent.py:252-260)
+    with parameters, moments and gradients resident on the device: no host
+    round trip inside the loop, one read-back at the end.  Same kernels and
+    rounding as the host-driven loop; a non-finite gradient rejects that
+    step and every later one (adam_step's rule) and raises its ValueError."""
+    b, n = state.batch, state.num_nodes
+    k = params.embed_dim
+    dtype = np.dtype(params.dtype)
+    actions = np.asarray(actions, dtype=np.int64)
+    targets = np.asarray(targets, dtype=dtype)
+    if actions.shape != (b,) or targets.shape != (b,):
+        raise ValueError(f"need {b} actions and targets, got {actions.shape} and {targets.shape}")
+    if not np.all(np.isfinite(targets)):
+        raise ValueError("targets must be finite")
+    if np.any(actions < 0) or np.any(actions >= n):
+        raise ValueError("action node index out of range")
+    _check_dtype(state, params)
+    dev = state.device
+    dparams = _DeviceParams(params, dev)
+    tdt = _torch_dtype(dtype)
+    m_d = torch.from_numpy(np.ascontiguousarray(flatten_arrays(adam.m), dtype=dtype)).to(dev)
+    v_d = torch.from_numpy(np.ascontiguousarray(flatten_arrays(adam.v), dtype=dtype)).to(dev)
+    npar = m_d.numel()
+    bad = torch.zeros(max(tau, 1), dtype=torch.int32, device=dev)
+    losses = torch.zeros(max(tau, 1), dtype=torch.float64, device=dev)
+    pack = None
+    for it in range(tau):
+        pack = _loss_pack(state, actions, targets, params, dparams, comm)
+        losses[it:it + 1].copy_(pack[-1:])
+        step = adam.step + it + 1
+        _lib.call("s2v_adam_pack", _dt_code(dtype), dparams.buf.data_ptr(), ptr(pack), ptr(m_d),
+                  ptr(v_d), npar, adam.beta1, 1 - adam.beta1, adam.beta2, 1 - adam.beta2,
+                  adam.eps, adam.lr, 1.0 - adam.beta1 ** step, 1.0 - adam.beta2 ** step,
+                  ptr(bad), it, stream_ptr())
+    if tau <= 0:
+        return []
+    flags = bad.to("cpu").numpy()
+    done = int(np.argmax(flags != 0)) if flags.any() else tau
+    new_p = dparams.buf.to("cpu").numpy().astype(dtype)
+    for name, arr in unflatten_arrays(new_p, k).items():
+        getattr(params, name)[...] = arr
+    for name, arr in unflatten_arrays(m_d.to("cpu").numpy(), k).items():
+        adam.m[name] = arr
+    for name, arr in unflatten_arrays(v_d.to("cpu").numpy(), k).items():
+        adam.v[name] = arr
+    adam.step += done
+    dparams._flat = np.ascontiguousarray(flatten_arrays(params.as_dict()), dtype=dtype)
+    if done < tau:
+        grads = unflatten_arrays(pack.to("cpu").numpy()[:-1].astype(dtype), k)
+        name = next(nm for nm in PARAM_NAMES if not np.all(np.isfinite(grads[nm])))
+        raise ValueError(f"non-finite gradient for {name}; step rejected")
+    return [float(x) / b for x in losses.to("cpu").numpy()[:tau]]
 
 
 # ---------------------------------------------------------------------------

@@ -120,6 +120,24 @@ def _structure(graph: Graph, part: Partition, device: torch.device) -> _ShardStr
     return st
 
 
+def _assemble(dev, dtype: torch.dtype, total: int, segments) -> torch.Tensor:
+    """dst[off + i] = src[skip + i] + add for segments (src, off, len, add[, skip])
+    in one s2v_segment_copy launch."""
+    out = torch.empty(max(total, 1), dtype=dtype, device=dev)
+    elem = out.element_size()
+    table = np.zeros((len(segments), 4), dtype=np.int64)
+    for i, sg in enumerate(segments):
+        src, off, n, add = sg[:4]
+        skip = sg[4] if len(sg) > 4 else 0
+        table[i] = (src.data_ptr() + skip * elem, off, n, add)
+    longest = int(table[:, 2].max()) if len(segments) else 0
+    if longest:
+        segs = to_device(table.reshape(-1), dev, pinned=True)
+        _lib.call("s2v_segment_copy", elem, ptr(segs), len(segments), longest, ptr(out),
+                  stream_ptr())
+    return out
+
+
 class PartitionedState:
     """One rank's slice of state for a batch of B graphs with equal N
     (state.py:56-111), resident in HBM."""
@@ -166,26 +184,36 @@ class PartitionedState:
             self.cols = s0.cols0.clone()
             self.order = s0.order if rows else torch.zeros(1, dtype=torch.int32, device=dev)
         else:
-            # block-diagonal assembly over slots (device-to-device, structure cached)
-            rp = [s.row_ptr[:-1] + int(ent_off[b]) for b, s in enumerate(structs)]
-            rp.append(torch.tensor([self.nnz], dtype=torch.int64, device=dev))
-            self.row_ptr = torch.cat(rp)
-            self.cols = torch.cat([s.cols0 + int(b * slot_stride) if b else s.cols0.clone()
-                                   for b, s in enumerate(structs)]) if self.nnz else \
-                torch.zeros(1, dtype=torch.int32, device=dev)
-            cp = [s.col_ptr[:-1] + int(ent_off[b]) for b, s in enumerate(structs)]
-            cp.append(torch.tensor([self.nnz], dtype=torch.int64, device=dev))
-            self.col_ptr = torch.cat(cp)
-            self.col_ent = torch.cat([s.col_ent + int(ent_off[b])
-                                      for b, s in enumerate(structs)]) \
-                if self.nnz else torch.zeros(1, dtype=torch.int64, device=dev)
-            self.col_row = torch.cat([s.col_row + int(b * rows) for b, s in enumerate(structs)]) \
-                if self.nnz else torch.zeros(1, dtype=torch.int32, device=dev)
+            # block-diagonal assembly over slots (device-to-device, structure
+            # cached): one segment-copy launch per array
+            e = [int(x) for x in ent_off]
+            lp = int(structs[0].col_ptr.numel())
+            self.row_ptr = _assemble(dev, torch.int64, batch * rows + 1, [
+                (s.row_ptr, b * rows, rows + (1 if b == batch - 1 else 0), e[b])
+                for b, s in enumerate(structs)])
+            self.col_ptr = _assemble(dev, torch.int64, batch * (lp - 1) + 1, [
+                (s.col_ptr, b * (lp - 1), lp - (0 if b == batch - 1 else 1), e[b])
+                for b, s in enumerate(structs)])
+            if self.nnz:
+                self.cols = _assemble(dev, torch.int32, self.nnz, [
+                    (s.cols0, e[b], s.nnz, b * slot_stride) for b, s in enumerate(structs)])
+                self.col_ent = _assemble(dev, torch.int64, self.nnz, [
+                    (s.col_ent, e[b], s.nnz, e[b]) for b, s in enumerate(structs)])
+                self.col_row = _assemble(dev, torch.int32, self.nnz, [
+                    (s.col_row, e[b], s.nnz, b * rows) for b, s in enumerate(structs)])
+            else:
+                self.cols = torch.zeros(1, dtype=torch.int32, device=dev)
+                self.col_ent = torch.zeros(1, dtype=torch.int64, device=dev)
+                self.col_row = torch.zeros(1, dtype=torch.int32, device=dev)
             # hub rows of every slot first, then the remaining rows of every slot
             if rows:
-                self.order = torch.cat(
-                    [s.order[:s.n_hub] + int(b * rows) for b, s in enumerate(structs)] +
-                    [s.order[s.n_hub:] + int(b * rows) for b, s in enumerate(structs)])
+                hubs = np.cumsum([0] + [s.n_hub for s in structs])
+                rest = np.cumsum([0] + [rows - s.n_hub for s in structs])
+                segs = [(s.order, int(hubs[b]), s.n_hub, b * rows)
+                        for b, s in enumerate(structs)]
+                segs += [(s.order, int(hubs[-1] + rest[b]), rows - s.n_hub, b * rows, s.n_hub)
+                         for b, s in enumerate(structs)]
+                self.order = _assemble(dev, torch.int32, batch * rows, segs)
             else:
                 self.order = torch.zeros(1, dtype=torch.int32, device=dev)
         self.n_hub = sum(s.n_hub for s in structs)

@@ -132,3 +132,63 @@ def test_tensor_core_backward_path_vs_port():
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+def test_device_tau_loop_equals_host_loop():
+    """train_step's device-resident tau loop (policy.train_iterations) gives
+    the parameters, moments, step count and losses of the host-driven
+    loss_and_gradients + adam_step loop, bit for bit."""
+    from paper_2105_08764_b200.policy import train_iterations
+    gs = [P.generate_ba(3000, 4, 40 + i) for i in range(4)]
+    rng = np.random.default_rng(3)
+    sol = (rng.random((4, 3000)) < 0.1).astype(np.uint8)
+    targets = rng.normal(size=4).astype(np.float32)
+
+    def run(device_loop):
+        def worker(comm):
+            part = P.partition_rows(3000, 1)[0]
+            st = P.PartitionedState(gs, part, solutions=sol)
+            acts = np.array([int(np.flatnonzero(st.cand[b])[7]) for b in range(4)])
+            params = P.PolicyParams.initialize(64, 5, seed=2)
+            adam = P.AdamState.create(params, lr=1e-3)
+            if device_loop:
+                losses = train_iterations(st, acts, targets, params, adam, 3, comm)
+            else:
+                losses = []
+                for _ in range(3):
+                    loss, grads = P.loss_and_gradients(st, acts, targets, params, comm)
+                    P.adam_step(params, grads, adam)
+                    losses.append(loss)
+            return losses, params.as_dict(), adam.m, adam.v, adam.step
+        return P.run_workers(1, worker)[0]
+
+    got, want = run(True), run(False)
+    assert got[0] == want[0] and got[4] == want[4] == 3
+    for a, b in zip(got[1:4], want[1:4]):
+        for name in P.PARAM_NAMES:
+            assert np.array_equal(a[name], b[name]), name
+
+
+def test_device_tau_loop_rejects_non_finite():
+    """A target that overflows the gradients: the step is rejected (params,
+    moments and step count untouched) with adam_step's ValueError."""
+    from paper_2105_08764_b200.policy import train_iterations
+    g = P.generate_ba(2000, 4, 5)
+
+    def worker(comm):
+        part = P.partition_rows(2000, 1)[0]
+        st = P.PartitionedState([g], part)
+        params = P.PolicyParams.initialize(64, 5, seed=0)
+        before = {k: v.copy() for k, v in params.as_dict().items()}
+        adam = P.AdamState.create(params, lr=1e-3)
+        act = np.array([int(np.flatnonzero(st.cand[0])[0])])
+        try:
+            train_iterations(st, act, np.array([3e38], np.float32), params, adam, 2, comm)
+        except ValueError as e:
+            msg = str(e)
+        else:
+            msg = ""
+        same = all(np.array_equal(before[k], v) for k, v in params.as_dict().items())
+        return msg, same, adam.step
+    msg, same, step = P.run_workers(1, worker)[0]
+    assert "non-finite gradient" in msg and same and step == 0
