@@ -162,7 +162,11 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
   __shared__ __align__(16) float ms[kTileRows][64 + 4];  // m tile
   __shared__ int32_t s_rows[kTileRows];
   __shared__ int64_t s_e0[kTileRows], s_e1[kTileRows];  // neighbour range, empty if in S
-  __shared__ int s_tile;
+  __shared__ int32_t s_trow[kTileRows];                 // e12 table row (sol, rdeg)
+  // next tile fetched one tile ahead: its index (atomic) and its rows' ids
+  // (cp.async, no registers held) overlap the current tile's projection
+  __shared__ int32_t s_raw[2][kTileRows];
+  __shared__ int s_tiles[2];
   bool have_theta = false;  // staged with the first tile (idle CTAs skip it)
   const int tid = threadIdx.x;
   const int hw = tid >> 4, sub = tid & 15;  // half-warp id, lane in half-warp
@@ -175,29 +179,47 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
   const int64_t nrows = sh.active ? sh.active_n[0] : (int64_t)sh.batch * sh.num_rows;
   const int64_t first = sh.active ? sh.active_n[1] : (sh.order ? sh.n_hub : 0);
   const int64_t ntiles = (nrows - first + kTileRows - 1) / kTileRows;
+  // row ids of tile t into s_raw[buf] (thread tid < kTileRows: row tid)
+  auto prefetch_rows = [&](int64_t t, int buf) {
+    const int64_t q = first + t * kTileRows + tid;
+    if (t < ntiles && q < nrows && list)
+      cp_async4(&s_raw[buf][tid], list + q);
+    else
+      s_raw[buf][tid] = (t < ntiles && q < nrows) ? (int32_t)q : -1;
+  };
+  if (tid == 0) s_tiles[0] = atomicAdd(tile_counter, 1);
+  __syncthreads();
+  if (tid < kTileRows) prefetch_rows(s_tiles[0], 0);
+  int cur = 0;
   for (;;) {
+    cp_async_wait_all();
     __syncthreads();
-    if (tid == 0) s_tile = atomicAdd(tile_counter, 1);
-    __syncthreads();
-    const int64_t tile = s_tile;
+    const int64_t tile = s_tiles[cur];
     if (tile >= ntiles) break;
+    if (tid == 0) s_tiles[cur ^ 1] = atomicAdd(tile_counter, 1);
     if (!have_theta) {  // visible to the projection after the gather's barrier
       for (int idx = tid; idx < 64 * 64; idx += blockDim.x) thT[idx % 64][idx / 64] = theta4[idx];
       have_theta = true;
     }
     if (tid < kTileRows) {
-      // one pass loads every row's id, range and membership in S
+      // one pass loads every row's range, membership in S and e12 row
       const int64_t q = first + tile * kTileRows + tid;
-      const int32_t r = q < nrows ? (list ? list[q] : (int32_t)q) : -1;
+      const int32_t r = s_raw[cur][tid];
       s_rows[tid] = r;
       int64_t e0 = 0, e1 = 0;
-      if (r >= 0 && h_in && !sh.sol[r]) {
-        // the active list's compact CSR is indexed by list position
-        e0 = sh.active_ptr ? sh.active_ptr[q] : sh.row_ptr[r];
-        e1 = sh.active_ptr ? sh.active_ptr[q + 1] : sh.row_ptr[r + 1];
+      int trow = 0;
+      if (r >= 0) {
+        const bool in_s = sh.sol[r] != 0;
+        trow = in_s ? max_deg + 1 : sh.rdeg[r];
+        if (h_in && !in_s) {
+          // the active list's compact CSR is indexed by list position
+          e0 = sh.active_ptr ? sh.active_ptr[q] : sh.row_ptr[r];
+          e1 = sh.active_ptr ? sh.active_ptr[q + 1] : sh.row_ptr[r + 1];
+        }
       }
       s_e0[tid] = e0;
       s_e1[tid] = e1;
+      s_trow[tid] = trow;
     }
     __syncthreads();
     // ---- gather: each half-warp handles rows hw and hw+16 of the tile
@@ -215,6 +237,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       if (m_out && r >= 0) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
     }
     __syncthreads();
+    if (tid < kTileRows) prefetch_rows(s_tiles[cur ^ 1], cur ^ 1);
     // ---- projection: thread -> rows {rp, rp+16}, k in [4*kq, 4*kq+4)
     const int kq = tid & 15, rp = tid >> 4;
     float z[2][4];
@@ -240,7 +263,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       const int64_t r = s_rows[rp + 16 * a];
       if (r < 0) continue;
       const int64_t b = r / sh.num_rows, i = r - b * sh.num_rows;
-      const int trow = sh.sol[r] ? max_deg + 1 : sh.rdeg[r];
+      const int trow = s_trow[rp + 16 * a];
       const float4 e = *reinterpret_cast<const float4 *>(table + (int64_t)trow * 64 + kq * 4);
       float4 o;
       o.x = relu(__fadd_rn(e.x, z[a][0]));
@@ -253,6 +276,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       for (int q = 0; q < npeers; q++)
         if (peers[q] != h_out) *reinterpret_cast<float4 *>(peers[q] + phys * 64 + kq * 4) = o;
     }
+    cur ^= 1;
   }
 }
 

@@ -39,6 +39,15 @@ __device__ __forceinline__ uint32_t ldg_u32_pol(const uint32_t *ptr, uint64_t po
   return v;
 }
 
+// 4-byte global -> shared copy without a register round trip
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 __device__ __forceinline__ void add4(float4 &a, const float4 &b) {
   a.x = __fadd_rn(a.x, b.x);
   a.y = __fadd_rn(a.y, b.y);
