@@ -791,14 +791,36 @@ __global__ void __launch_bounds__(256) gather64_kernel(s2v_shard sh,
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
   const int64_t nhw = ((int64_t)gridDim.x * blockDim.x) >> 4;
   const int64_t first = sh.order ? sh.n_hub : 0;  // hub rows: hub_gather64_kernel
-  for (int64_t q = first + (((int64_t)blockIdx.x * blockDim.x + tid) >> 4); q < nrows; q += nhw) {
-    const int64_t r = sh.order ? sh.order[q] : q;
+  // two-deep software pipeline over this half-warp's rows q, q+nhw, ...:
+  // the row id two rows ahead and the range / S bit of the next row are
+  // loaded before the current row's gather, so they arrive during it
+  auto row_of = [&](int64_t qq) -> int64_t {
+    return qq < nrows ? (sh.order ? (int64_t)sh.order[qq] : qq) : -1;
+  };
+  int64_t q = first + (((int64_t)blockIdx.x * blockDim.x + tid) >> 4);
+  int64_t rA = row_of(q), rB = row_of(q + nhw);
+  int64_t a0 = 0, a1 = 0;
+  if (rA >= 0 && !sh.sol[rA]) {
+    a0 = sh.row_ptr[rA];
+    a1 = sh.row_ptr[rA + 1];
+  }
+  for (; q < nrows; q += nhw) {
+    const int64_t rC = row_of(q + 2 * nhw);
+    int64_t b0 = 0, b1 = 0;
+    if (rB >= 0 && !sh.sol[rB]) {
+      b0 = sh.row_ptr[rB];
+      b1 = sh.row_ptr[rB + 1];
+    }
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (!sh.sol[r])
-      acc = gather_row64(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, src, sub, hmask, hbase,
-                         hot_rows, pol_hot, pol_cold, nullptr, nullptr,
-                         (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
-    st4(out + r * 64 + 4 * sub, acc);
+    if (a1 > a0)
+      acc = gather_row64(a0, a1, sh.cols, src, sub, hmask, hbase, hot_rows, pol_hot, pol_cold,
+                         nullptr, nullptr,
+                         (uint32_t)((rA / sh.num_rows) * sh.world * sh.rows_max));
+    st4(out + rA * 64 + 4 * sub, acc);
+    rA = rB;
+    rB = rC;
+    a0 = b0;
+    a1 = b1;
   }
 }
 
