@@ -382,23 +382,29 @@ __global__ void __launch_bounds__(256, 2) layer_backward64_kernel(
       p4[a][c] = first ? 0.f : partial[(int64_t)blockIdx.x * 4096 + (4 * lo + a) * 64 + 4 * hi + c];
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
   const int64_t ntiles = (nrows + kT64 - 1) / kT64;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * kT64;
-    __syncthreads();
-    float4 G[kT64 / 16], H[kT64 / 16], O[kT64 / 16], M[kT64 / 16];
+  // register double buffer: the next tile's grad_h / h_l / dzsum / m_l
+  // loads are issued right after the current tile is staged in shared
+  // memory, so they fly during its dzT m and dz theta4 products
+  float4 G[kT64 / 16], H[kT64 / 16], O[kT64 / 16], M[kT64 / 16];
+  auto load_tile = [&](int64_t t) {
 #pragma unroll
     for (int q = 0; q < kT64 / 16; q++) {  // every load in flight before any use
       const int e = tid + q * 256, row = e >> 4, c4 = e & 15;
-      const int64_t r = r0 + row;
+      const int64_t r = t * kT64 + row;
       const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
       G[q] = H[q] = O[q] = M[q] = z4;
-      if (r < nrows) {
+      if (t < ntiles && r < nrows) {
         G[q] = f4(grad_h + r * 64 + 4 * c4);
         H[q] = f4(h_l + phys_of_row(sh, r) * 64 + 4 * c4);
         if (!first) O[q] = f4(dzsum + r * 64 + 4 * c4);
         if (m_l) M[q] = f4(m_l + r * 64 + 4 * c4);
       }
     }
+  };
+  load_tile(blockIdx.x);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kT64;
+    __syncthreads();
 #pragma unroll
     for (int q = 0; q < kT64 / 16; q++) {
       const int e = tid + q * 256, row = e >> 4, c4 = e & 15;
@@ -414,6 +420,7 @@ __global__ void __launch_bounds__(256, 2) layer_backward64_kernel(
       st4(&dzs[row][4 * c4], dz);
       st4(&ms[row][4 * c4], M[q]);
     }
+    load_tile(tile + gridDim.x);
     __syncthreads();
     if (m_l) {
 #pragma unroll 4
