@@ -164,14 +164,22 @@ int s2v_embed_round_peers(s2v_dtype dt, const s2v_shard *sh, const void *theta4,
  * K = 64 fp32. */
 int s2v_h1_table(s2v_dtype dt, const void *theta4, const void *table, int K, int max_deg,
                  void *h1_table, void *stream);
-/* Embedding round 2 at P = 1 without reading h1: round 1's output row of an
- * alive neighbour u (never in S) is h1_table[rdeg[u]], so the gather reads
- * the L1/L2-resident table instead of the 256-byte rows of h1.  Same result
- * bits as s2v_embed_round(h_in = h1).  Replaces the second iteration of
- * policy.py:163-174.  K = 64 fp32, world = 1. */
+/* Embedding round 2 without reading h1: round 1's output row of an alive
+ * neighbour u (never in S) is h1_table[rdeg[u]], so the gather reads the
+ * L1/L2-resident table instead of the 256-byte rows of h1, and round 1 needs
+ * no halo exchange.  Same result bits as s2v_embed_round(h_in = h1).
+ * deg_phys: residual degree by physical row of every rank (s2v_trow, then
+ * the same all-gather as an embedding buffer with K = 1); NULL at P = 1
+ * (this shard's rdeg).  peer_outs/npeers as s2v_embed_round_peers (fused
+ * push of h2).  Replaces the second iteration of policy.py:163-174.
+ * K = 64 fp32. */
 int s2v_embed_round2_table(s2v_dtype dt, const s2v_shard *sh, const void *theta4,
                            const void *table, int K, int max_deg, const void *h1_table,
-                           void *h_out, void *m_out, void *stream);
+                           const int32_t *deg_phys, void *h_out, void *const *peer_outs,
+                           int npeers, void *m_out, void *stream);
+/* trow_phys[(b*P + rank)*rows_max + i] = sol ? max_deg + 1 : rdeg for this
+ * rank's rows (the e12 table row of each node). */
+int s2v_trow(const s2v_shard *sh, int max_deg, int32_t *trow_phys, void *stream);
 
 /* Stable in-place compaction of an active-row list: keeps the rows of
  * list[0, n[0]) with rdeg > 0, in order, and updates n = {rows, rows among

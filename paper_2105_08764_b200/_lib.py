@@ -68,7 +68,8 @@ _SIGNATURES = {
     "s2v_e12_table": ([_I, _P, _P, _P, _I, _I, _P, _P], _I),
     "s2v_embed_round": ([_I, _SH, _P, _P, _I, _I, _P, _P, _P, _P], _I),
     "s2v_h1_table": ([_I, _P, _P, _I, _I, _P, _P], _I),
-    "s2v_embed_round2_table": ([_I, _SH, _P, _P, _I, _I, _P, _P, _P, _P], _I),
+    "s2v_embed_round2_table": ([_I, _SH, _P, _P, _I, _I, _P, _P, _P, _P, _I, _P, _P], _I),
+    "s2v_trow": ([_SH, _I, _P, _P], _I),
     "s2v_embed_round_peers": ([_I, _SH, _P, _P, _I, _I, _P, _P, _P, _I, _P, _P], _I),
     "s2v_colsum": ([_I, _SH, _I, _P, _P, _P, _SZ, _P], _I),
     "s2v_colsum_workspace": ([_SH, _I, _I], _SZ),

@@ -157,7 +157,9 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
     s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ table, int max_deg,
     const float *__restrict__ h_in, float *__restrict__ h_out, float *__restrict__ m_out,
     int *__restrict__ tile_counter, uint32_t hot_rows, float *const *__restrict__ peers,
-    int npeers) {
+    int npeers, const int32_t *__restrict__ deg_src) {
+  // deg_src (TABLE): residual degree by physical row -- every rank's rows
+  // at P > 1 (s2v_trow + exchange), this shard's rdeg at P = 1
   __shared__ __align__(16) float thT[64][64 + 4];        // thT[p][k] = theta4[k][p]
   __shared__ __align__(16) float ms[kTileRows][64 + 4];  // m tile
   __shared__ int32_t s_rows[kTileRows];
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       if (s_e1[lr] > s_e0[lr])
         acc = gather_row64<TABLE>(
             s_e0[lr], s_e1[lr], sh.active_ptr ? sh.active_cols : sh.cols, h_in, sub, hmask, hbase,
-            hot_rows, pol_hot, pol_cold, sh.rdeg, sh.active_ptr ? sh.sol : nullptr,
+            hot_rows, pol_hot, pol_cold, deg_src, sh.active_ptr ? sh.sol : nullptr,
             TABLE ? 0u : (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
       *reinterpret_cast<float4 *>(&ms[lr][sub * 4]) = acc;
       if (m_out && r >= 0) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
@@ -288,7 +290,8 @@ template <bool TABLE>
 __global__ void __launch_bounds__(256, 1) hub_round64_kernel(
     s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ table, int max_deg,
     const float *__restrict__ h_in, float *__restrict__ h_out, float *__restrict__ m_out,
-    int *__restrict__ counter, uint32_t hot_rows, float *const *__restrict__ peers, int npeers) {
+    int *__restrict__ counter, uint32_t hot_rows, float *const *__restrict__ peers, int npeers,
+    const int32_t *__restrict__ deg_src) {
   extern __shared__ __align__(16) float hub_smem[];
   float *ring = hub_smem;                              // [2][120][64]
   float(*thT)[65] = reinterpret_cast<float(*)[65]>(hub_smem + 2 * kHubBatch * 64);
@@ -312,10 +315,10 @@ __global__ void __launch_bounds__(256, 1) hub_round64_kernel(
     if (h_in && !sh.sol[r]) {
       if (sh.active_ptr)
         acc = hub_gather_row64<TABLE>(sh.active_ptr[q], sh.active_ptr[q + 1], sh.active_cols,
-                                      h_in, ring, hot_rows, pol_hot, pol_cold, sh.rdeg, sh.sol);
+                                      h_in, ring, hot_rows, pol_hot, pol_cold, deg_src, sh.sol);
       else
         acc = hub_gather_row64<TABLE>(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, h_in, ring,
-                                      hot_rows, pol_hot, pol_cold, sh.rdeg);
+                                      hot_rows, pol_hot, pol_cold, deg_src);
     }
     if (tid < 16) {
       *reinterpret_cast<float4 *>(mrow + sub * 4) = acc;
@@ -1221,11 +1224,13 @@ template <class T>
 static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *table, int K,
                          int max_deg, const void *h_in, void *h_out, void *m_out,
                          cudaStream_t st, float *const *peers = nullptr, int npeers = 0,
-                         bool from_table = false) {
+                         bool from_table = false, const int32_t *deg_phys = nullptr) {
   const int64_t nrows = (int64_t)sh->batch * sh->num_rows;
   if (nrows == 0) return S2V_OK;
-  if (from_table && !(sizeof(T) == 4 && K == 64 && sh->world == 1 && !npeers))
-    return fail(S2V_EINVAL, "degree-table rounds need K = 64 fp32 at P = 1");
+  if (from_table && !(sizeof(T) == 4 && K == 64 && (sh->world == 1 || deg_phys)))
+    return fail(S2V_EINVAL, "degree-table rounds need K = 64 fp32 (and every rank's degrees "
+                            "at P > 1)");
+  const int32_t *deg_src = deg_phys ? deg_phys : sh->rdeg;
   if (sh->active && !(sizeof(T) == 4 && K == 64 && sh->world == 1 && sh->batch == 1))
     return fail(S2V_EINVAL, "active-row lists need K = 64 fp32, B = 1, P = 1");
   if (sizeof(T) == 4 && K == 64) {
@@ -1252,12 +1257,12 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
       int hgrid = (int)std::min<int64_t>(sh->n_hub, kNumSMs);
       hub_kern<<<hgrid, 256, kHubSmem, hs>>>(
           *sh, (const float *)theta4, (const float *)table, max_deg, (const float *)h_in,
-          (float *)h_out, (float *)m_out, hub_counter, hot_rows, peers, npeers);
+          (float *)h_out, (float *)m_out, hub_counter, hot_rows, peers, npeers, deg_src);
     }, &ss);
     if (rc) return rc;
     kern<<<grid, 256, 0, st>>>(*sh, (const float *)theta4, (const float *)table, max_deg,
                                (const float *)h_in, (float *)h_out, (float *)m_out, counter,
-                               hot_rows, peers, npeers);
+                               hot_rows, peers, npeers, deg_src);
     S2V_LAUNCH_CHECK();
     if (ss) S2V_CUDA_CHECK(cudaStreamWaitEvent(st, ss->done, 0));
     S2V_LAUNCH_CHECK();
@@ -1352,10 +1357,31 @@ int s2v_h1_table(s2v_dtype dt, const void *theta4, const void *table, int K, int
 
 int s2v_embed_round2_table(s2v_dtype dt, const s2v_shard *sh, const void *theta4,
                            const void *table, int K, int max_deg, const void *h1_table,
-                           void *h_out, void *m_out, void *stream) {
-  if (dt != S2V_F32) return fail(S2V_EINVAL, "degree-table rounds need K = 64 fp32 at P = 1");
+                           const int32_t *deg_phys, void *h_out, void *const *peer_outs,
+                           int npeers, void *m_out, void *stream) {
+  if (dt != S2V_F32) return fail(S2V_EINVAL, "degree-table rounds need K = 64 fp32");
   return embed_round_t<float>(sh, theta4, table, K, max_deg, h1_table, h_out, m_out,
-                              as_stream(stream), nullptr, 0, true);
+                              as_stream(stream), (float *const *)peer_outs, npeers, true,
+                              deg_phys);
+}
+
+// trow[phys row] = sol ? max_deg + 1 : rdeg for this rank's rows
+__global__ void trow_kernel(s2v_shard sh, int max_deg, int32_t *__restrict__ trow) {
+  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = r / sh.num_rows, i = r - b * sh.num_rows;
+    trow[(b * sh.world + sh.rank) * sh.rows_max + i] = sh.sol[r] ? max_deg + 1 : sh.rdeg[r];
+  }
+}
+
+int s2v_trow(const s2v_shard *sh, int max_deg, int32_t *trow_phys, void *stream) {
+  const int64_t nrows = (int64_t)sh->batch * sh->num_rows;
+  if (nrows == 0) return S2V_OK;
+  trow_kernel<<<(int)std::min<int64_t>((nrows + 255) / 256, kNumSMs * 8), 256, 0,
+                as_stream(stream)>>>(*sh, max_deg, trow_phys);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
 }
 
 int s2v_embed_round(s2v_dtype dt, const s2v_shard *sh, const void *theta4, const void *table,

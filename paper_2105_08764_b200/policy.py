@@ -254,11 +254,15 @@ def _allgather_rows(state: PartitionedState, comm, h: torch.Tensor, k: int, tag:
 ROUND_TIMER = None
 
 
-def _degree_table_round2(state: PartitionedState, k: int, dt: int, num_layers: int) -> bool:
+def _degree_table_round2(state: PartitionedState, k: int, dt: int, num_layers: int,
+                         tape: bool = False) -> bool:
     """Round 2 from the per-degree table of round-1 outputs (s2v_h1_table +
-    s2v_embed_round2_table): K = 64 fp32 at P = 1.  S2V_DEG_TABLE=0 turns it
-    off (the plain round reading h1 gives the same bits)."""
-    return (state.world == 1 and k == 64 and dt == _lib.S2V_F32 and num_layers >= 2
+    s2v_embed_round2_table): K = 64 fp32; at P > 1 for inference (the ranks
+    exchange 4-byte residual degrees instead of 256-byte h1 rows).
+    S2V_DEG_TABLE=0 turns it off (the plain round reading h1 gives the same
+    bits)."""
+    return (k == 64 and dt == _lib.S2V_F32 and num_layers >= 2
+            and (state.world == 1 or not tape)
             and os.environ.get("S2V_DEG_TABLE", "1") != "0")
 
 
@@ -296,7 +300,7 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
     h_prev = None
     out = []
     h1t = None
-    if _degree_table_round2(state, k, dt, num_layers):
+    if _degree_table_round2(state, k, dt, num_layers, tape):
         h1t = state.workspace("h1t", (k, max_deg), lambda: torch.empty(
             (max_deg + 2) * k, dtype=torch.float32, device=state.device))
         if not reuse:
@@ -318,8 +322,30 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
             out.append(None)
             continue
         if h1t is not None and layer == 1:
+            deg = None
+            peers = None
+            dc = comm.device_comm() if state.world > 1 else None
+            if dc is not None:
+                # every rank's residual degrees by physical row (4 B per node
+                # instead of the 256-byte h1 rows a plain round 2 gathers)
+                deg = state.workspace("trow", state.batch * state.world * state.rows_max,
+                                      lambda: torch.zeros(
+                                          max(state.batch * state.world * state.rows_max, 1),
+                                          dtype=torch.int32, device=state.device))
+                _lib.call("s2v_trow", state.shard_ref(), max_deg, ptr(deg), st)
+                _allgather_rows(state, comm, deg, 1, "trow", name="trow")
+                if dc.supports_push:
+                    peers = _peer_list(state, dc, f"h{layer % 2}/{len(hs)}", h_out, True)
             _lib.call("s2v_embed_round2_table", dt, state.shard_ref(), dparams.ptr("theta4"),
-                      ptr(table), k, max_deg, ptr(h1t), ptr(h_out), ptr(m_out), st)
+                      ptr(table), k, max_deg, ptr(h1t), ptr(deg), ptr(h_out), ptr(peers),
+                      state.world if peers is not None else 0, ptr(m_out), st)
+            if dc is not None:
+                if peers is not None:
+                    dc.signal_and_wait(st)
+                    comm.record("embed_fwd", state.rows_max * k * state.batch)
+                else:
+                    _allgather_rows(state, comm, h_out, k, "embed_fwd",
+                                    name=f"h{layer % 2}/{len(hs)}")
             sh.active, sh.active_n, sh.active_ptr, sh.active_cols = outer
             h_prev = h_out
             out.append(h_out)

@@ -97,6 +97,9 @@ class _ShardStructure:
         self.nnz = hi - lo
         self.rows = rows
         self.max_deg = int(np.diff(row_ptr).max()) if rows else 0
+        # over the whole graph: e12 / h1 tables are indexed by the residual
+        # degree of neighbours that other ranks own
+        self.max_deg_global = int(np.diff(row_ptr_g).max()) if n else 0
         # descending-degree processing order (load balance of the round
         # kernel); rows above the hub degree go to the CTA-cooperative kernel
         deg = np.diff(row_ptr)
@@ -170,7 +173,7 @@ class PartitionedState:
         self.rows_max = rows_max_of(n, P)
         rows = part.num_rows
         structs = [_structure(g, part, dev) for g in graphs]
-        self.max_deg = max(s.max_deg for s in structs)
+        self.max_deg = max(s.max_deg_global for s in structs)
         ent_off = np.zeros(batch + 1, dtype=np.int64)
         np.cumsum([s.nnz for s in structs], out=ent_off[1:])
         self.nnz = int(ent_off[-1])
