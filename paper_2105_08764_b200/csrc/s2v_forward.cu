@@ -1303,6 +1303,18 @@ __global__ void dead_rows_kernel(const T *__restrict__ h1_table, int K, int max_
   }
 }
 
+// ed[e] = degree of entry e's neighbour (removed entries keep their bit):
+// the table row round 2 gathers for that entry
+__global__ void edge_degree_kernel(const uint32_t *__restrict__ cols,
+                                   const int32_t *__restrict__ deg, int64_t nnz,
+                                   uint32_t *__restrict__ ed) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = cols[e];
+    ed[e] = (c & S2V_DEAD) ? c : (uint32_t)__ldg(deg + c);
+  }
+}
+
 }  // namespace s2v
 
 using namespace s2v;
@@ -1360,6 +1372,41 @@ int s2v_embed_round2_table(s2v_dtype dt, const s2v_shard *sh, const void *theta4
                            const int32_t *deg_phys, void *h_out, void *const *peer_outs,
                            int npeers, void *m_out, void *stream) {
   if (dt != S2V_F32) return fail(S2V_EINVAL, "degree-table rounds need K = 64 fp32");
+  static const bool edge_pass = [] {
+    const char *e = getenv("S2V_EDGE_DEG");
+    return !(e && e[0] == '0');
+  }();
+  // a table too large for L1 reuse (hub degrees nearly unique per hub: R-MAT
+  // scale 22 has a 41 MB table) is read from L2 either way; there the
+  // dependent degree lookup per neighbour is the cost, so it moves into a
+  // separate streaming pass (measured: 3.86 -> 3.0 + 0.43 ms at R-MAT scale
+  // 22; at BA(2M,16), 2.4 MB table, the in-gather lookup is 0.2 ms faster)
+  const bool big_table = (int64_t)(max_deg + 2) * 256 > (8ll << 20);
+  if (edge_pass && big_table && K == 64 && !sh->active_ptr && sh->nnz > 0 &&
+      (sh->world == 1 || deg_phys)) {
+    // stream pass: every entry's neighbour degree (random 4-byte reads with
+    // full memory-level parallelism), then a plain round over those table
+    // indices -- the round's gather loses its dependent degree lookup
+    static thread_local uint32_t *ed = nullptr;
+    static thread_local int64_t cap = 0;
+    static thread_local int ed_dev = -1;
+    int dev = 0;
+    S2V_CUDA_CHECK(cudaGetDevice(&dev));
+    if (sh->nnz > cap || dev != ed_dev) {
+      if (ed && dev == ed_dev) S2V_CUDA_CHECK(cudaFree(ed));
+      S2V_CUDA_CHECK(cudaMalloc(&ed, sizeof(uint32_t) * sh->nnz));
+      cap = sh->nnz;
+      ed_dev = dev;
+    }
+    cudaStream_t st = as_stream(stream);
+    edge_degree_kernel<<<(int)std::min<int64_t>((sh->nnz + 255) / 256, kNumSMs * 8), 256, 0,
+                         st>>>(sh->cols, deg_phys ? deg_phys : sh->rdeg, sh->nnz, ed);
+    S2V_LAUNCH_CHECK();
+    s2v_shard e = *sh;
+    e.cols = ed;
+    return embed_round_t<float>(&e, theta4, table, K, max_deg, h1_table, h_out, m_out, st,
+                                (float *const *)peer_outs, npeers, false, nullptr);
+  }
   return embed_round_t<float>(sh, theta4, table, K, max_deg, h1_table, h_out, m_out,
                               as_stream(stream), (float *const *)peer_outs, npeers, true,
                               deg_phys);

@@ -92,3 +92,22 @@ def test_degree_table_round2_equals_plain_round(make, monkeypatch):
     rp, cols = gs[1].csr_arrays()
     h_o = cref.forward(rp, cols, sol[1], params.as_dict(), 5)[0]
     assert np.array_equal(h_t[1].T, h_o)  # (scores at B > 1 follow the batched u1 order)
+
+
+def test_big_table_edge_degree_pass_bitwise(monkeypatch):
+    """A degree table above 8 MB (a 40,000-leaf star: max degree > 32K)
+    takes the streaming edge-degree pass before round 2; embeddings and
+    scores stay bitwise equal to the oracle and to the in-gather lookup."""
+    base = P.generate_ba(50000, 4, 8)
+    star = np.stack([np.full(40000, 3), np.arange(10000, 50000)], axis=1)
+    g = P.Graph(50000, np.concatenate([base.edge_array, star]))
+    rp, cols = g.csr_arrays()
+    assert (int(np.diff(rp).max()) + 2) * 256 > 8 << 20
+    params = P.PolicyParams.initialize(64, 5, seed=4)
+    sol = (np.random.default_rng(5).random(g.num_nodes) < 0.02).astype(np.uint8)
+    monkeypatch.setenv("S2V_EDGE_DEG", "1")
+    h_gpu, s_gpu, cand_gpu = _forward_gpu(g, params, sol)
+    h, _, _, cand, sc = cref.forward(rp, cols, sol, params.as_dict(), 5)
+    assert np.array_equal(cand_gpu, cand)
+    assert np.array_equal(h_gpu, h)
+    assert np.array_equal(s_gpu, sc)
