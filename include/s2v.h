@@ -339,6 +339,39 @@ int s2v_adam_pack(s2v_dtype dt, void *params, const double *pack, void *m, void 
                   double beta1, double omb1, double beta2, double omb2, double eps, double lr,
                   double b1c, double b2c, int32_t *bad, int it, void *stream);
 
+/* ---- one whole policy evaluation of the selection loop ------------------- */
+/* The device episode loop's evaluation (inference.py:107-147) as ONE call:
+ * rounds (round 2 from the degree table when h1_table is set), global sum,
+ * u1, scores and top-d keys, the d rule and picks, the group apply and the
+ * trace row c -- the same entry points in the same order as the host-driven
+ * sequence, without a host call per launch.  P = 1, fp32, no active list;
+ * the e12 table (and h1 table) must be current for the packed theta. */
+typedef struct {
+  int K, L, max_deg, dmax;
+  const float *theta;        /* theta1..theta7 packed as param_shapes (device) */
+  const float *table;        /* e12 table */
+  const float *h1_table;     /* NULL: round 1 runs and round 2 reads h1      */
+  float *h[2];               /* ping-pong embedding buffers                  */
+  void *colsum_ws;
+  size_t colsum_ws_bytes;
+  float *g, *u1, *scores;
+  uint64_t *block_keys;
+  int64_t *out;              /* counts [B], then top keys [B][dmax][2]       */
+  const double *fracs;       /* host: schedule thresholds (s2v_select)       */
+  const int *ds;
+  int nthr, fallback;
+  uint8_t *active;
+  int64_t *picks;
+  int32_t *evaluated, *error;
+  int64_t *info;
+  uint8_t *applied;
+  int64_t *removed;
+  int64_t *t_picks;          /* [chunk][B*dmax]; row c written                */
+  uint8_t *t_applied;        /* [chunk][B*dmax]                               */
+  int32_t *t_eval;           /* [chunk][B]                                    */
+} s2v_eval_plan;
+int s2v_eval_chain(const s2v_shard *sh, const s2v_eval_plan *plan, int c, void *stream);
+
 /* ---- graph ingestion (graphs.py:125-157) --------------------------------- */
 /* Bit-exact generate_ba from numpy's PCG64 state {state_hi, state_lo, inc_hi,
  * inc_lo, has_uint32, uinteger} (host memory).  edges_out == NULL returns E. */

@@ -21,6 +21,18 @@ TOPK_MAX = 8
 HUB_DEGREE = 4096  # include/s2v.h S2V_HUB_DEGREE
 
 
+class s2v_eval_plan(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_int), ("L", ctypes.c_int), ("max_deg", ctypes.c_int),
+                ("dmax", ctypes.c_int)] + [(f, ctypes.c_void_p) for f in (
+                    "theta", "table", "h1_table", "h0", "h1", "colsum_ws")] + [
+                ("colsum_ws_bytes", ctypes.c_size_t)] + [(f, ctypes.c_void_p) for f in (
+                    "g", "u1", "scores", "block_keys", "out", "fracs", "ds")] + [
+                ("nthr", ctypes.c_int), ("fallback", ctypes.c_int)] + [
+                (f, ctypes.c_void_p) for f in (
+                    "active", "picks", "evaluated", "error", "info", "applied", "removed",
+                    "t_picks", "t_applied", "t_eval")]
+
+
 class s2v_shard(ctypes.Structure):
     _fields_ = [
         ("num_nodes", ctypes.c_int64),
@@ -89,6 +101,7 @@ _SIGNATURES = {
     "s2v_topk_below": ([_SH, _P, _P, _P, _P], _I),
     "s2v_u1": ([_I, _I, _I, _P, _P, _P, _P], _I),
     "s2v_u1_exact": ([_I, _I], _I),
+    "s2v_eval_chain": ([_SH, ctypes.POINTER(s2v_eval_plan), _I, _P], _I),
     "s2v_select": ([_I, _I, _I64, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P], _I),
     "s2v_trace": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     "s2v_backward_blocks": ([_SH], _I),
@@ -170,6 +183,10 @@ KERNELS_PER_CALL = {
     "s2v_grad_h_init": 1, "s2v_layer_backward": 1, "s2v_gather": 1, "s2v_param_grads": 1,
     "s2v_reduce_partials": 1, "s2v_head_backward": 1, "s2v_adam": 1,
     "s2v_u1": 1, "s2v_select": 1, "s2v_trace": 1,
+    "s2v_h1_table": 1, "s2v_embed_round2_table": 1, "s2v_trow": 1, "s2v_colsum_residual": 3,
+    "s2v_active_compact": 3, "s2v_score_cached": 2, "s2v_frontier_seed": 3,
+    "s2v_frontier_expand": 9, "s2v_adam_pack": 2, "s2v_segment_copy": 1,
+    "s2v_eval_chain": 14,  # L = 5: 4 rounds, colsum 2, u1, score, merge, select, apply 3, trace
 }
 launch_count = 0
 

@@ -145,4 +145,46 @@ int s2v_trace(int B, int dmax, const int64_t *picks, const uint8_t *applied,
   return S2V_OK;
 }
 
+int s2v_eval_chain(const s2v_shard *sh, const s2v_eval_plan *p, int c, void *stream) {
+  if (sh->world != 1 || sh->active) return fail(S2V_EINVAL, "eval chain: P = 1, no active list");
+  const int K = p->K, B = sh->batch, d = p->dmax;
+  if (d < 1 || d > 8 || p->L < 1) return fail(S2V_EINVAL, "eval chain: bad plan");
+  const float *th = p->theta;
+  const float *t4 = th + 2 * K + K * K, *t5 = t4 + K * K, *t6 = t5 + K * K, *t7 = t6 + K * K;
+  int rc;
+  // rounds (policy._forward_rounds, inference: ping-pong buffers)
+  const float *h_prev = nullptr;
+  for (int layer = 0; layer < p->L; layer++) {
+    float *h_out = p->h[layer % 2];
+    if (p->h1_table && layer == 0) continue;  // nothing reads h1 but round 2
+    if (p->h1_table && layer == 1)
+      rc = s2v_embed_round2_table(S2V_F32, sh, t4, p->table, K, p->max_deg, p->h1_table, nullptr,
+                                  h_out, nullptr, 0, nullptr, stream);
+    else
+      rc = s2v_embed_round(S2V_F32, sh, t4, p->table, K, p->max_deg, h_prev, h_out, nullptr,
+                           stream);
+    if (rc) return rc;
+    h_prev = h_out;
+  }
+  // global sum, u1, scores, top-d keys (policy._score)
+  if ((rc = s2v_colsum(S2V_F32, sh, K, h_prev, p->g, p->colsum_ws, p->colsum_ws_bytes, stream)))
+    return rc;
+  if ((rc = s2v_u1(S2V_F32, B, K, p->g, t5, p->u1, stream))) return rc;
+  if ((rc = s2v_score(S2V_F32, sh, K, h_prev, p->u1, t6, t7, nullptr, 0, p->scores,
+                      p->block_keys, p->out, stream)))
+    return rc;
+  uint64_t *top = (uint64_t *)(p->out + B);
+  if ((rc = s2v_topk_merge(sh, p->block_keys, d, top, stream))) return rc;
+  // d rule + picks, group apply, trace (inference.DeviceEpisode._launch_one)
+  if ((rc = s2v_select(B, d, sh->num_nodes, p->fracs, p->ds, p->nthr, p->fallback, p->out, top,
+                       p->active, p->picks, p->evaluated, p->error, stream)))
+    return rc;
+  if ((rc = s2v_apply_phase1(sh, p->picks, d, p->info, 0, nullptr, stream))) return rc;
+  if ((rc = s2v_apply_phase2(sh, p->picks, d, p->info, p->applied, p->removed, 1, stream)))
+    return rc;
+  return s2v_trace(B, d, p->picks, p->applied, p->evaluated, sh->residual, p->active,
+                   p->t_picks + (int64_t)c * B * d, p->t_applied + (int64_t)c * B * d,
+                   p->t_eval + (int64_t)c * B, stream);
+}
+
 }  // extern "C"

@@ -1382,7 +1382,9 @@ int s2v_embed_round2_table(s2v_dtype dt, const s2v_shard *sh, const void *theta4
   // separate streaming pass (measured: 3.86 -> 3.0 + 0.43 ms at R-MAT scale
   // 22; at BA(2M,16), 2.4 MB table, the in-gather lookup is 0.2 ms faster)
   const bool big_table = (int64_t)(max_deg + 2) * 256 > (8ll << 20);
-  if (edge_pass && big_table && K == 64 && !sh->active_ptr && sh->nnz > 0 &&
+  // (whole-graph rounds only: an active list or frontier visits few rows,
+  // and the pass would touch every entry)
+  if (edge_pass && big_table && K == 64 && !sh->active && sh->nnz > 0 &&
       (sh->world == 1 || deg_phys)) {
     // stream pass: every entry's neighbour degree (random 4-byte reads with
     // full memory-level parallelism), then a plain round over those table
