@@ -831,6 +831,73 @@ __global__ void __launch_bounds__(256) gather64_kernel(s2v_shard sh,
   }
 }
 
+// spmm_t, tiled like round64_kernel: 32-row tiles in descending-degree
+// order from an atomic counter, the next tile's index and row ids fetched
+// during the current tile's gathers (cp.async), two rows per half-warp.
+constexpr int kGTile = 32;
+
+__global__ void __launch_bounds__(256, 4) gather64_tiles_kernel(s2v_shard sh,
+                                                                const float *__restrict__ src,
+                                                                float *__restrict__ out,
+                                                                uint32_t hot_rows,
+                                                                int *__restrict__ tile_counter) {
+  __shared__ int32_t s_raw[2][kGTile];
+  __shared__ int64_t s_e0[kGTile], s_e1[kGTile];
+  __shared__ int32_t s_rows[kGTile];
+  __shared__ int s_tiles[2];
+  const int tid = threadIdx.x, hw = tid >> 4, sub = tid & 15;
+  const unsigned hmask = (tid & 16) ? 0xFFFF0000u : 0x0000FFFFu;
+  const int hbase = tid & 16;
+  const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
+  const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  const int64_t first = sh.order ? sh.n_hub : 0;  // hub rows: hub_gather64_kernel
+  const int64_t ntiles = (nrows - first + kGTile - 1) / kGTile;
+  auto prefetch_rows = [&](int64_t t, int buf) {
+    const int64_t q = first + t * kGTile + tid;
+    if (t < ntiles && q < nrows && sh.order)
+      cp_async4(&s_raw[buf][tid], sh.order + q);
+    else
+      s_raw[buf][tid] = (t < ntiles && q < nrows) ? (int32_t)q : -1;
+  };
+  if (tid == 0) s_tiles[0] = atomicAdd(tile_counter, 1);
+  __syncthreads();
+  if (tid < kGTile) prefetch_rows(s_tiles[0], 0);
+  int cur = 0;
+  for (;;) {
+    cp_async_wait_all();
+    __syncthreads();
+    const int64_t tile = s_tiles[cur];
+    if (tile >= ntiles) break;
+    if (tid == 0) s_tiles[cur ^ 1] = atomicAdd(tile_counter, 1);
+    if (tid < kGTile) {
+      const int32_t r = s_raw[cur][tid];
+      s_rows[tid] = r;
+      int64_t e0 = 0, e1 = 0;
+      if (r >= 0 && !sh.sol[r]) {
+        e0 = sh.row_ptr[r];
+        e1 = sh.row_ptr[r + 1];
+      }
+      s_e0[tid] = e0;
+      s_e1[tid] = e1;
+    }
+    __syncthreads();
+    if (tid < kGTile) prefetch_rows(s_tiles[cur ^ 1], cur ^ 1);
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      const int lr = hw + 16 * q;
+      const int64_t r = s_rows[lr];
+      if (r < 0) continue;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (s_e1[lr] > s_e0[lr])
+        acc = gather_row64(s_e0[lr], s_e1[lr], sh.cols, src, sub, hmask, hbase, hot_rows,
+                           pol_hot, pol_cold, nullptr, nullptr,
+                           (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
+      st4(out + r * 64 + 4 * sub, acc);
+    }
+    cur ^= 1;
+  }
+}
+
 // spmm_t of the hub rows: one CTA per row, cooperative gather.
 __global__ void __launch_bounds__(256, 1) hub_gather64_kernel(s2v_shard sh,
                                                               const float *__restrict__ src,
@@ -974,7 +1041,26 @@ int s2v_gather(s2v_dtype dt, const s2v_shard *sh, int K, const void *src, void *
       int rc = hub_gather_launch(sh, (const float *)src, (float *)out, hot, st, &side, &done);
       if (rc) return rc;
     }
-    gather64_kernel<<<kNumSMs * 8, 256, 0, st>>>(*sh, (const float *)src, (float *)out, hot);
+    static const bool tiles = [] {
+      const char *e = getenv("S2V_GATHER_TILES");
+      return !(e && e[0] == '0');
+    }();
+    if (tiles) {
+      static thread_local int *counter = nullptr;
+      static thread_local int counter_dev = -1;
+      int dev = 0;
+      S2V_CUDA_CHECK(cudaGetDevice(&dev));
+      if (counter_dev != dev) {
+        S2V_CUDA_CHECK(cudaMalloc(&counter, sizeof(int)));
+        counter_dev = dev;
+      }
+      S2V_CUDA_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), st));
+      const int64_t ntiles = (rows + kGTile - 1) / kGTile;
+      gather64_tiles_kernel<<<(int)std::min<int64_t>(std::max<int64_t>(ntiles, 1), kNumSMs * 4),
+                              256, 0, st>>>(*sh, (const float *)src, (float *)out, hot, counter);
+    } else {
+      gather64_kernel<<<kNumSMs * 8, 256, 0, st>>>(*sh, (const float *)src, (float *)out, hot);
+    }
     S2V_LAUNCH_CHECK();
     if (done) S2V_CUDA_CHECK(cudaStreamWaitEvent(st, done, 0));
     return S2V_OK;
