@@ -701,20 +701,39 @@ __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
   }
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
   const int64_t ntiles = (nrows + kT64 - 1) / kT64;
+  // register double buffer: the next tile's dz sums and (S bit, degree) are
+  // loaded while the current tile's products run
+  float4 D[kT64 * 16 / 256];
+  uint8_t nsol = 0;
+  int32_t ndeg = 0;
+  auto load_tile = [&](int64_t t) {
+#pragma unroll
+    for (int q = 0; q < kT64 * 16 / 256; q++) {
+      const int e = tid + q * 256, row = e >> 4, c4 = e & 15;
+      const int64_t r = t * kT64 + row;
+      D[q] = (t < ntiles && r < nrows) ? f4(dzsum + r * 64 + 4 * c4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (tid < kT64) {
+      const int64_t r = t * kT64 + tid;
+      const bool ok = t < ntiles && r < nrows;
+      nsol = ok ? sh.sol[r] : 0;
+      ndeg = ok ? sh.rdeg[r] : 0;
+    }
+  };
+  load_tile(blockIdx.x);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * kT64;
     __syncthreads();
     if (tid < kT64) {
-      const int64_t r = r0 + tid;
-      const bool ok = r < nrows;
-      s_sol[tid] = (ok && sh.sol[r]) ? 1.f : 0.f;
-      s_deg[tid] = (ok && !sh.sol[r]) ? (float)sh.rdeg[r] : 0.f;
+      s_sol[tid] = nsol ? 1.f : 0.f;
+      s_deg[tid] = nsol ? 0.f : (float)ndeg;
     }
     __syncthreads();
-    for (int e = tid; e < kT64 * 16; e += 256) {
+#pragma unroll
+    for (int q = 0; q < kT64 * 16 / 256; q++) {
+      const int e = tid + q * 256;
       const int row = e >> 4, c4 = e & 15;
-      const int64_t r = r0 + row;
-      const float4 d = r < nrows ? f4(dzsum + r * 64 + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 d = D[q];
       st4(&dzs[row][4 * c4], d);
       const float deg = s_deg[row];
       float4 w;
@@ -725,6 +744,7 @@ __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
       st4(&ws[row][4 * c4], w);
     }
     __syncthreads();
+    load_tile(tile + gridDim.x);
     // dtheta3[k][j] += dz[row][k] w[row][j]   (k = 4lo+a, j = 4hi+c)
 #pragma unroll 4
     for (int row = 0; row < kT64; row++) {
