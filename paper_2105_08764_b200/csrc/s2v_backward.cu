@@ -53,6 +53,30 @@ __global__ void grad_h_init_kernel(s2v_shard sh, int K, const T *__restrict__ dg
   }
 }
 
+// K = 64 fp32: one float4 per thread, slot from the grid's y (no integer
+// division per element); a thread's column quad is fixed (stride % 16 == 0)
+__global__ void grad_h_init64_kernel(s2v_shard sh, const float *__restrict__ dg,
+                                     const int64_t *__restrict__ actions,
+                                     const float *__restrict__ dact, float *__restrict__ grad_h) {
+  const int b = blockIdx.y, c4 = threadIdx.x & 15;
+  const float4 g = reinterpret_cast<const float4 *>(dg + (int64_t)b * 64)[c4];
+  const int64_t act = actions[b] - sh.row_start;  // local row of the action, if owned
+  const int64_t n4 = sh.num_rows * 16;
+  float4 *out = reinterpret_cast<float4 *>(grad_h + (int64_t)b * sh.num_rows * 64);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = g;
+    if ((q >> 4) == act) {
+      const float4 a = reinterpret_cast<const float4 *>(dact + (int64_t)b * 64)[c4];
+      v.x = __fadd_rn(v.x, a.x);
+      v.y = __fadd_rn(v.y, a.y);
+      v.z = __fadd_rn(v.z, a.z);
+      v.w = __fadd_rn(v.w, a.w);
+    }
+    out[q] = v;
+  }
+}
+
 // Layer backward over tiles of kBwdTile local rows.
 //   dz = grad_h * (h_l > 0); dzsum += dz; P4 += dz (x) m_l; dm = theta4^T dz
 template <class T>
@@ -1028,7 +1052,12 @@ int s2v_grad_h_init(s2v_dtype dt, const s2v_shard *sh, int K, const void *dg,
   int64_t total = (int64_t)sh->batch * sh->num_rows * K;
   if (total == 0) return S2V_OK;
   int grid = (int)std::min<int64_t>((total + 255) / 256, kNumSMs * 8);
-  if (dt == S2V_F32)
+  if (dt == S2V_F32 && K == 64) {
+    const int gx = (int)std::max<int64_t>(
+        1, std::min<int64_t>((sh->num_rows * 16 + 255) / 256, kNumSMs * 8 / sh->batch + 1));
+    grad_h_init64_kernel<<<dim3(gx, sh->batch), 256, 0, as_stream(stream)>>>(
+        *sh, (const float *)dg, actions, (const float *)dact, (float *)grad_h);
+  } else if (dt == S2V_F32)
     grad_h_init_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(
         *sh, K, (const float *)dg, actions, (const float *)dact, (float *)grad_h);
   else
