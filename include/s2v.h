@@ -372,6 +372,18 @@ typedef struct {
 } s2v_eval_plan;
 int s2v_eval_chain(const s2v_shard *sh, const s2v_eval_plan *plan, int c, void *stream);
 
+/* P > 1 device loop helpers.  gathered = every rank's score read-back
+ * vector (counts [B], then top-d keys [B][d][2]) as [P][B*(1+2d)] after a
+ * device all-gather; out = the global counts and top-d keys in the same
+ * layout, identical on every rank (replaces policy.merge_rank_keys, the host
+ * all_gather of keys, inference.py:113).  s2v_sum_ranks: out = sum over the
+ * P gathered rows of n int64 (the group-apply info, in rank order).
+ * s2v_sub_i64: a -= b (the global residual after a group apply). */
+int s2v_merge_rank_keys(int P, int B, int d, const int64_t *gathered, int64_t *out,
+                        void *stream);
+int s2v_sum_ranks(int P, int64_t n, const int64_t *gathered, int64_t *out, void *stream);
+int s2v_sub_i64(int64_t *a, const int64_t *b, int n, void *stream);
+
 /* ---- graph ingestion (graphs.py:125-157) --------------------------------- */
 /* Bit-exact generate_ba from numpy's PCG64 state {state_hi, state_lo, inc_hi,
  * inc_lo, has_uint32, uinteger} (host memory).  edges_out == NULL returns E. */

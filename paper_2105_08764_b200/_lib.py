@@ -101,6 +101,9 @@ _SIGNATURES = {
     "s2v_topk_below": ([_SH, _P, _P, _P, _P], _I),
     "s2v_u1": ([_I, _I, _I, _P, _P, _P, _P], _I),
     "s2v_u1_exact": ([_I, _I], _I),
+    "s2v_merge_rank_keys": ([_I, _I, _I, _P, _P, _P], _I),
+    "s2v_sum_ranks": ([_I, _I64, _P, _P, _P], _I),
+    "s2v_sub_i64": ([_P, _P, _I, _P], _I),
     "s2v_eval_chain": ([_SH, ctypes.POINTER(s2v_eval_plan), _I, _P], _I),
     "s2v_select": ([_I, _I, _I64, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P], _I),
     "s2v_trace": ([_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I),
@@ -186,6 +189,7 @@ KERNELS_PER_CALL = {
     "s2v_h1_table": 1, "s2v_embed_round2_table": 1, "s2v_trow": 1, "s2v_colsum_residual": 3,
     "s2v_active_compact": 3, "s2v_score_cached": 2, "s2v_frontier_seed": 3,
     "s2v_frontier_expand": 9, "s2v_adam_pack": 2, "s2v_segment_copy": 1,
+    "s2v_merge_rank_keys": 1, "s2v_sum_ranks": 1, "s2v_sub_i64": 1,
     "s2v_eval_chain": 14,  # L = 5: 4 rounds, colsum 2, u1, score, merge, select, apply 3, trace
 }
 launch_count = 0

@@ -7,6 +7,8 @@
 //   u1 = g @ theta5.T                      pkg/src/graphrl/policy.py:201
 //   SelectionSchedule.d_for / select_top_d pkg/src/graphrl/inference.py:54-73,116-124
 //   active = residual_counts > 0           pkg/src/graphrl/inference.py:147
+#include <algorithm>
+
 #include "s2v_common.cuh"
 
 namespace s2v {
@@ -100,6 +102,53 @@ __global__ void trace_kernel(int B, int dmax, const int64_t *__restrict__ picks,
   }
 }
 
+// P > 1 device loop: the ranks' (counts, top-d keys) gathered as
+// [P][B*(1 + 2d)] int64 -> the global counts and top-d keys, same layout,
+// identically on every rank (merge_rank_keys' order: key, then ~node).
+__global__ void merge_rank_keys_kernel(int P, int B, int d, const int64_t *__restrict__ g,
+                                       int64_t *__restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int64_t len = (int64_t)B * (1 + 2 * d);
+  int64_t cnt = 0;
+  Key top[8];
+  for (int q = 0; q < 8; q++) top[q] = null_key();
+  for (int r = 0; r < P; r++) {
+    const int64_t *src = g + r * len;
+    cnt += src[b];
+    const Key *k = reinterpret_cast<const Key *>(src + B) + (int64_t)b * d;
+    for (int j = 0; j < d; j++) {
+      const Key x = k[j];
+      if (!key_gt(x, top[d - 1])) continue;
+      int pos = d - 1;
+      while (pos > 0 && key_gt(x, top[pos - 1])) {
+        top[pos] = top[pos - 1];
+        pos--;
+      }
+      top[pos] = x;
+    }
+  }
+  out[b] = cnt;
+  Key *o = reinterpret_cast<Key *>(out + B) + (int64_t)b * d;
+  for (int j = 0; j < d; j++) o[j] = top[j];
+}
+
+// out[i] = sum over ranks of g[r][i], ascending rank order
+__global__ void sum_ranks_kernel(int P, int64_t n, const int64_t *__restrict__ g,
+                                 int64_t *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = 0;
+    for (int r = 0; r < P; r++) s += g[r * n + i];
+    out[i] = s;
+  }
+}
+
+__global__ void sub_i64_kernel(int64_t *__restrict__ a, const int64_t *__restrict__ b, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] -= b[i];
+}
+
 }  // namespace s2v
 
 using namespace s2v;
@@ -185,6 +234,29 @@ int s2v_eval_chain(const s2v_shard *sh, const s2v_eval_plan *p, int c, void *str
   return s2v_trace(B, d, p->picks, p->applied, p->evaluated, sh->residual, p->active,
                    p->t_picks + (int64_t)c * B * d, p->t_applied + (int64_t)c * B * d,
                    p->t_eval + (int64_t)c * B, stream);
+}
+
+int s2v_merge_rank_keys(int P, int B, int d, const int64_t *gathered, int64_t *out,
+                        void *stream) {
+  if (P < 1 || B < 1 || d < 1 || d > 8) return fail(S2V_EINVAL, "bad key merge args");
+  merge_rank_keys_kernel<<<(B + 63) / 64, 64, 0, as_stream(stream)>>>(P, B, d, gathered, out);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_sum_ranks(int P, int64_t n, const int64_t *gathered, int64_t *out, void *stream) {
+  if (n <= 0) return S2V_OK;
+  sum_ranks_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, as_stream(stream)>>>(
+      P, n, gathered, out);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_sub_i64(int64_t *a, const int64_t *b, int n, void *stream) {
+  if (n <= 0) return S2V_OK;
+  sub_i64_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(a, b, n);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
 }
 
 }  // extern "C"
