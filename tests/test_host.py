@@ -164,3 +164,19 @@ def test_gloo_world2_host_protocol():
         # broken by lowest index: nodes 1, 2
         assert nodes == [4, 1, 2]
         assert counts == [6]
+
+
+def test_bench_peak_parser(tmp_path, monkeypatch):
+    """bench.py's roofline peak: a sustained HBM figure from the
+    driver-written MEASURED_PEAKS.json when present (GB/s or TB/s), else the
+    profiling recipe's fallback."""
+    import bench
+    f = tmp_path / "MEASURED_PEAKS.json"
+    monkeypatch.setattr(bench, "MEASURED", f)
+    assert bench.peaks()[0] == 6650.0
+    f.write_text('{"hbm": {"burst_gbs": 7400, "sustained_gbs": 6900}, "bf16_tflops": 2200}')
+    assert bench.peaks()[0] == 6900.0
+    f.write_text('{"copy_bandwidth_tbs": 6.8}')
+    assert bench.peaks()[0] == 6800.0
+    f.write_text('{"bf16_tflops": 2200}')
+    assert bench.peaks()[0] == 6650.0
