@@ -395,6 +395,9 @@ __global__ void __launch_bounds__(256, 2) layer_backward64_kernel(
   float(*th4)[68] = reinterpret_cast<float(*)[68]>(smem_f);
   float(*dzs)[68] = reinterpret_cast<float(*)[68]>(smem_f + 64 * 68);
   float(*ms)[68] = reinterpret_cast<float(*)[68]>(smem_f + 2 * 64 * 68);
+  // dz transposed, dzT[k][row] with 4-row groups XOR-swizzled by (k>>2)&7:
+  // the dm product reads 4 rows of one k as one float4
+  float *dzT = smem_f + 3 * 64 * 68;
   const int tid = threadIdx.x;
   for (int idx = tid; idx < 64 * 64; idx += 256) th4[idx / 64][idx % 64] = theta4[idx];
   const int lo = tid & 15, hi = tid >> 4;
@@ -443,6 +446,13 @@ __global__ void __launch_bounds__(256, 2) layer_backward64_kernel(
                                                  O[q].w + dz.w));
       st4(&dzs[row][4 * c4], dz);
       st4(&ms[row][4 * c4], M[q]);
+      if (dm_out) {
+        const int rsw = row ^ ((c4 & 7) << 2);
+        dzT[(4 * c4 + 0) * 64 + rsw] = dz.x;
+        dzT[(4 * c4 + 1) * 64 + rsw] = dz.y;
+        dzT[(4 * c4 + 2) * 64 + rsw] = dz.z;
+        dzT[(4 * c4 + 3) * 64 + rsw] = dz.w;
+      }
     }
     load_tile(tile + gridDim.x);
     __syncthreads();
@@ -467,9 +477,11 @@ __global__ void __launch_bounds__(256, 2) layer_backward64_kernel(
 #pragma unroll 4
       for (int k = 0; k < 64; k++) {
         const float4 t = f4(&th4[k][4 * lo]);
+        const float4 d4 = f4(&dzT[k * 64 + ((4 * hi) ^ (((k >> 2) & 7) << 2))]);
+        const float dv4[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
         for (int a = 0; a < 4; a++) {
-          const float d = dzs[4 * hi + a][k];
+          const float d = dv4[a];
           acc[a][0] = __fmaf_rn(t.x, d, acc[a][0]);
           acc[a][1] = __fmaf_rn(t.y, d, acc[a][1]);
           acc[a][2] = __fmaf_rn(t.z, d, acc[a][2]);
@@ -1019,7 +1031,7 @@ static int layer_backward_t(const s2v_shard *sh, int K, const void *theta4, cons
     return S2V_OK;
   }
   if (sizeof(T) == 4 && K == 64) {
-    const size_t smem = sizeof(float) * 3 * 64 * 68;
+    const size_t smem = sizeof(float) * (3 * 64 * 68 + 64 * 64);
     S2V_CUDA_CHECK(cudaFuncSetAttribute(layer_backward64_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     layer_backward64_kernel<<<bwd_blocks(*sh), 256, smem, st>>>(
