@@ -309,9 +309,20 @@ int s2v_layer_backward(s2v_dtype dt, const s2v_shard *sh, int K, const void *the
 int s2v_gather(s2v_dtype dt, const s2v_shard *sh, int K, const void *src, void *out,
                void *stream);
 /* Partials [blk][2K + K*K] of dtheta1, dtheta2, dtheta3 from dzsum
- * (policy.py:294-296,305-306; dw_acc = theta3^T dzsum by linearity). */
+ * (policy.py:294-296,305-306; dw_acc = theta3^T dzsum by linearity).
+ * t2c (optional, s2v_theta2_terms_bytes) receives the einsum terms
+ * fl(fl(dw_acc * (w > 0)) * deg) of policy.py:305-306 in the chain layout
+ * [b][ceil(K/G)][rows][G], G = 32 / sizeof(T), for s2v_theta2_einsum. */
 int s2v_param_grads(s2v_dtype dt, const s2v_shard *sh, int K, const void *theta2,
-                    const void *theta3, const void *dzsum, void *partials, void *stream);
+                    const void *theta3, const void *dzsum, void *partials, void *t2c,
+                    void *stream);
+size_t s2v_theta2_terms_bytes(s2v_dtype dt, const s2v_shard *sh, int K);
+/* dtheta2 (policy.py:305-306) in numpy 2.3's einsum("bkv,bv->k") order:
+ * per (b, k), 16/sizeof(T) lane chains over v (4-vector unroll taken in
+ * reverse, zero-filled tail), lanes combined pairwise, slots added in b
+ * order.  tot: scratch [B][K] of T; out[K] (fp64) = this rank's dtheta2. */
+int s2v_theta2_einsum(s2v_dtype dt, const s2v_shard *sh, int K, const void *t2c, void *tot,
+                      double *out, void *stream);
 /* out[len] (fp64) = sum over nparts partial rows, fixed order. */
 int s2v_reduce_partials(s2v_dtype dt, const void *partials, int nparts, int len, double *out,
                         void *stream);

@@ -136,7 +136,34 @@ def kat_fixture(R):
     (OUT / "kat_dyadic.json").write_text(json.dumps(data, indent=1))
 
 
+def generator_fixture(R):
+    """SHA-256 of the reference generators' edge arrays (graphs.py:90-157),
+    so the native generate_ba / numpy generate_er are pinned bit for bit."""
+    import hashlib
+    out = {"source": "graphrl.generate_ba / generate_er (pkg/src/graphrl/graphs.py:90-157)",
+           "ba": [], "er": []}
+    for n, d, seed in ((1000, 4, 0), (20000, 4, 3), (100000, 16, 0)):
+        e = np.ascontiguousarray(R.generate_ba(n, d, seed).edge_array, dtype=np.int64)
+        out["ba"].append({"n": n, "d": d, "seed": seed, "edges": int(e.shape[0]),
+                          "sha256": hashlib.sha256(e.tobytes()).hexdigest()})
+    for n, rho, seed in ((300, 0.05, 7), (5000, 0.002, 1)):
+        e = np.ascontiguousarray(R.generate_er(n, rho, seed).edge_array, dtype=np.int64)
+        out["er"].append({"n": n, "rho": rho, "seed": seed, "edges": int(e.shape[0]),
+                          "sha256": hashlib.sha256(e.tobytes()).hexdigest()})
+    (OUT / "generators.json").write_text(json.dumps(out, indent=1))
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "gen":
+        generator_fixture(_ref())
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "cfg2":
+        # BASELINE configs[1]: 32 x BA(10000,4,seed=100+i), B=32, tau=4 (SURVEY 8(d))
+        R = _ref()
+        t0 = time.time()
+        train_fixture(R, "train_cfg2_ba10k_b32_k64_l5", 10000, 4, 32, 64, 5, 4)
+        print("cfg2", time.time() - t0)
+        return
     if os.environ.get("OPENBLAS_CORETYPE") != "SkylakeX":
         print("warning: set OPENBLAS_CORETYPE=SkylakeX for the pinned sgemm order")
     OUT.mkdir(parents=True, exist_ok=True)

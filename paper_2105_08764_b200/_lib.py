@@ -111,7 +111,9 @@ _SIGNATURES = {
     "s2v_grad_h_init": ([_I, _SH, _I, _P, _P, _P, _P, _P], _I),
     "s2v_layer_backward": ([_I, _SH, _I, _P, _P, _P, _P, _P, _P, _I, _P, _P], _I),
     "s2v_gather": ([_I, _SH, _I, _P, _P, _P], _I),
-    "s2v_param_grads": ([_I, _SH, _I, _P, _P, _P, _P, _P], _I),
+    "s2v_param_grads": ([_I, _SH, _I, _P, _P, _P, _P, _P, _P], _I),
+    "s2v_theta2_terms_bytes": ([_I, _SH, _I], _SZ),
+    "s2v_theta2_einsum": ([_I, _SH, _I, _P, _P, _P, _P], _I),
     "s2v_reduce_partials": ([_I, _P, _I, _I, _P, _P], _I),
     "s2v_head_backward": ([_I, _SH, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     "s2v_adam": ([_I, _P, _P, _P, _P, _I64, _D, _D, _D, _D, _D, _D, _D, _D, _P], _I),
@@ -184,7 +186,7 @@ KERNELS_PER_CALL = {
     "s2v_embed_round": 1, "s2v_embed_round_peers": 1, "s2v_colsum": 2, "s2v_score": 1, "s2v_topk_merge": 1, "s2v_score_keys": 1, "s2v_score_keys_f64": 1,
     "s2v_topk_below": 1,
     "s2v_grad_h_init": 1, "s2v_layer_backward": 1, "s2v_gather": 1, "s2v_param_grads": 1,
-    "s2v_reduce_partials": 1, "s2v_head_backward": 1, "s2v_adam": 1,
+    "s2v_reduce_partials": 1, "s2v_head_backward": 1, "s2v_adam": 1, "s2v_theta2_einsum": 2,
     "s2v_u1": 1, "s2v_select": 1, "s2v_trace": 1,
     "s2v_h1_table": 1, "s2v_embed_round2_table": 1, "s2v_trow": 1, "s2v_colsum_residual": 3,
     "s2v_active_compact": 3, "s2v_score_cached": 2, "s2v_frontier_seed": 3,

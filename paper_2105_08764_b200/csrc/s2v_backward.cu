@@ -169,7 +169,7 @@ __global__ void gather_kernel(s2v_shard sh, int K, const T *__restrict__ src,
 template <class T>
 __global__ void __launch_bounds__(kBwdThreads) param_grads_kernel(
     s2v_shard sh, int K, const T *__restrict__ theta2, const T *__restrict__ theta3,
-    const T *__restrict__ dzsum, T *__restrict__ partial) {
+    const T *__restrict__ dzsum, T *__restrict__ partial, T *__restrict__ t2c) {
   extern __shared__ unsigned char smem_raw[];
   T *th3 = reinterpret_cast<T *>(smem_raw);  // [K][K+1]
   T *dz_s = th3 + K * (K + 1);               // [tile][K]
@@ -215,10 +215,18 @@ __global__ void __launch_bounds__(kBwdThreads) param_grads_kernel(
       } else if (o < 2 * K) {  // dtheta2[j] = sum (theta3^T dz)_j * (w_j > 0) * deg
         const int j = o - K;
         for (int lr = 0; lr < kBwdTile; lr++) {
-          if (!(w_s[lr * K + j] > T(0))) continue;
+          const bool pos = w_s[lr * K + j] > T(0);
+          if (!pos && !t2c) continue;
           T dw = T(0);
           for (int k = 0; k < K; k++) dw = fmaT(th3[k * (K + 1) + j], dz_s[lr * K + k], dw);
-          a = fmaT(dw, aux[2 * lr + 1], a);
+          if (pos) a = fmaT(dw, aux[2 * lr + 1], a);
+          if (t2c && r0 + lr < nrows) {  // einsum term fl(fl(dw * (w > 0)) * deg)
+            const int64_t r = r0 + lr, b = r / sh.num_rows, v = r - b * sh.num_rows;
+            constexpr int G = 32 / sizeof(T);
+            const int ng = (K + G - 1) / G;
+            t2c[((b * ng + j / G) * sh.num_rows + v) * G + j % G] =
+                mulT(mulT(dw, pos ? T(1) : T(0)), aux[2 * lr + 1]);
+          }
         }
       } else {  // dtheta3[k][j] = sum dz_k w_j
         const int q = o - 2 * K, k = q / K, j = q - k * K;
@@ -230,6 +238,107 @@ __global__ void __launch_bounds__(kBwdThreads) param_grads_kernel(
   for (int t = 0; t < per && t < 72; t++) {
     int o = threadIdx.x + t * blockDim.x;
     if (o < LEN) partial[(int64_t)blockIdx.x * LEN + o] = acc[t];
+  }
+}
+
+// dtheta2 in numpy's einsum order (policy.py:305-306,
+// np.einsum("bkv,bv->k", dw_acc * (w > 0), deg)).  numpy 2.3's two-operand
+// reduction with an outstride-0 inner loop over v
+// (float/double_sum_of_products_contig_contig_outstride0_two, SSE baseline:
+// LANES = 16 / sizeof(T) lanes, 4-vector unroll applied in the order
+// v3, v2, v1, v0, mul then add, a zero-filled tail of LANES-wide vectors,
+// lanes combined as (a0 + a1) + (a2 + a3)) gives, for each (b, k), LANES
+// sequential chains over v; the per-b results are then added in b order.
+// The cancellation in this 4M-term sum at BA(2M,16) (|sum| << sum |term|)
+// makes it order-sensitive, so the device follows the same order
+// (pinned by tests/test_gpu_fullsize.py; emulated in oracle/port.py).
+// One CTA per (slot b, group of G = 32 / sizeof(T) columns): 3-stage cp.async
+// ring of kEinRows-row chunks of the chain layout, one warp runs the chains.
+constexpr int kEinRows = 1024;
+constexpr int kEinStages = 3;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) theta2_einsum_kernel(const T *__restrict__ t2c,
+                                                            int64_t rows, int K,
+                                                            T *__restrict__ tot) {
+  constexpr int G = 32 / sizeof(T), LANES = 16 / sizeof(T), BLK = 4 * LANES;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T *ring = reinterpret_cast<T *>(smem_raw);  // [kEinStages][kEinRows][G]
+  const int ng = (K + G - 1) / G;
+  const int b = blockIdx.x / ng, grp = blockIdx.x - b * ng;
+  const T *src = t2c + ((int64_t)b * ng + grp) * rows * G;
+  const int64_t nchunks = (rows + kEinRows - 1) / kEinRows;
+  auto issue = [&](int64_t c) {
+    if (c < nchunks) {
+      const int64_t base = c * kEinRows;
+      const int64_t n16 = ((rows - base < kEinRows ? rows - base : kEinRows) * G * sizeof(T)) / 16;
+      T *dst = ring + (c % kEinStages) * kEinRows * G;
+      for (int64_t e = threadIdx.x; e < n16; e += blockDim.x)
+        cp_async16(reinterpret_cast<char *>(dst) + 16 * e,
+                   reinterpret_cast<const char *>(src + base * G) + 16 * e);
+    }
+    cp_async_commit();
+  };
+  for (int c = 0; c < kEinStages - 1; c++) issue(c);
+  const int t = threadIdx.x;
+  const int lane = t / G, kin = t - lane * G;  // chain (kin, lane) in warp 0
+  const bool chain = t < G * LANES;
+  T acc = T(0);
+  const int64_t nfull = rows / BLK * BLK;  // rows in full 4-vector blocks
+  for (int64_t c = 0; c < nchunks; c++) {
+    issue(c + kEinStages - 1);
+    cp_async_wait<kEinStages - 1>();
+    __syncthreads();
+    if (chain) {
+      const T *s = ring + (c % kEinStages) * kEinRows * G;
+      const int64_t base = c * kEinRows;
+      const int64_t end = base + kEinRows < rows ? base + kEinRows : rows;
+      const int64_t fend = end < nfull ? end : nfull;
+      for (int64_t v0 = base; v0 < fend; v0 += BLK) {
+        const T *blk = s + (v0 - base) * G;
+#pragma unroll
+        for (int j = 3; j >= 0; j--) acc = addT(blk[(j * LANES + lane) * G + kin], acc);
+      }
+      for (int64_t v0 = fend > base ? fend : base; v0 < end; v0 += LANES) {  // tail
+        const int64_t v = v0 + lane;
+        acc = addT(v < end ? s[(v - base) * G + kin] : T(0), acc);
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  if (t < 32) {  // all of warp 0 (the chains, plus idle lanes for fp64)
+    // lanes of column kin sit in threads kin, kin + G, kin + 2G, ...
+    const unsigned full = 0xffffffffu;
+    T a1 = __shfl_down_sync(full, acc, G), a2 = T(0), a3 = T(0);
+    if (LANES == 4) {
+      a2 = __shfl_down_sync(full, acc, 2 * G);
+      a3 = __shfl_down_sync(full, acc, 3 * G);
+    }
+    if (chain && lane == 0 && grp * G + kin < K) {
+      const T r = LANES == 4 ? addT(addT(acc, a1), addT(a2, a3)) : addT(acc, a1);
+      tot[(int64_t)b * K + grp * G + kin] = r;
+    }
+  }
+}
+
+// out[k] = sum over slots b, in b order, of the per-slot chain results
+template <class T>
+__global__ void theta2_finish_kernel(const T *__restrict__ tot, int B, int K, double *out) {
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    T s = T(0);
+    for (int b = 0; b < B; b++) s = addT(s, tot[(int64_t)b * K + k]);
+    out[k] = (double)s;
   }
 }
 
@@ -717,7 +826,7 @@ __global__ void __launch_bounds__(256, 1) layer_backward64_tc_kernel(
 // Dynamic smem: th3 [64][68], dzs [64][68], ws [64][68], red [16][64], aux.
 __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
     s2v_shard sh, const float *__restrict__ theta2, const float *__restrict__ theta3,
-    const float *__restrict__ dzsum, float *__restrict__ partial) {
+    const float *__restrict__ dzsum, float *__restrict__ partial, float *__restrict__ t2c) {
   extern __shared__ __align__(16) float smem_f[];
   float(*th3)[68] = reinterpret_cast<float(*)[68]>(smem_f);
   float(*dzs)[68] = reinterpret_cast<float(*)[68]>(smem_f + 64 * 68);
@@ -818,6 +927,18 @@ __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
 #pragma unroll
         for (int c = 0; c < 4; c++)
           if (ws[row][4 * lo + c] > 0.f) p2[c] = __fmaf_rn(acc[a][c], deg, p2[c]);
+        const int64_t r = tile * kT64 + row;
+        if (t2c && r < nrows) {
+          // the einsum terms fl(fl(dw_acc * (w > 0)) * deg) of policy.py:305-306
+          // in the chain layout [b][k / 8][v][8] read by theta2_einsum_kernel
+          const int64_t b = r / sh.num_rows, v = r - b * sh.num_rows;
+          float t[4];
+#pragma unroll
+          for (int c = 0; c < 4; c++)
+            t[c] = __fmul_rn(__fmul_rn(acc[a][c], ws[row][4 * lo + c] > 0.f ? 1.f : 0.f), deg);
+          st4(t2c + ((b * 8 + (lo >> 1)) * sh.num_rows + v) * 8 + 4 * (lo & 1),
+              make_float4(t[0], t[1], t[2], t[3]));
+        }
       }
     }
     // dtheta1[k] += dz[row][k] sol[row]
@@ -1138,7 +1259,8 @@ int s2v_gather(s2v_dtype dt, const s2v_shard *sh, int K, const void *src, void *
 }
 
 int s2v_param_grads(s2v_dtype dt, const s2v_shard *sh, int K, const void *theta2,
-                    const void *theta3, const void *dzsum, void *partials, void *stream) {
+                    const void *theta3, const void *dzsum, void *partials, void *t2c,
+                    void *stream) {
   if (2 * K + K * K > 72 * kBwdThreads) return fail(S2V_EINVAL, "embed_dim %d too large", K);
   size_t elem = dt == S2V_F32 ? 4 : 8;
   size_t smem = elem * ((size_t)K * (K + 1) + 2 * kBwdTile * (size_t)K + 2 * kBwdTile);
@@ -1149,19 +1271,53 @@ int s2v_param_grads(s2v_dtype dt, const s2v_shard *sh, int K, const void *theta2
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64));
     param_grads64_kernel<<<bwd_blocks(*sh), 256, smem64, st>>>(
         *sh, (const float *)theta2, (const float *)theta3, (const float *)dzsum,
-        (float *)partials);
+        (float *)partials, (float *)t2c);
   } else if (dt == S2V_F32) {
     auto kern = param_grads_kernel<float>;
     S2V_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<bwd_blocks(*sh), kBwdThreads, smem, st>>>(*sh, K, (const float *)theta2,
                                                      (const float *)theta3,
-                                                     (const float *)dzsum, (float *)partials);
+                                                     (const float *)dzsum, (float *)partials,
+                                                     (float *)t2c);
   } else {
     auto kern = param_grads_kernel<double>;
     S2V_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<bwd_blocks(*sh), kBwdThreads, smem, st>>>(*sh, K, (const double *)theta2,
                                                      (const double *)theta3,
-                                                     (const double *)dzsum, (double *)partials);
+                                                     (const double *)dzsum, (double *)partials,
+                                                     (double *)t2c);
+  }
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+size_t s2v_theta2_terms_bytes(s2v_dtype dt, const s2v_shard *sh, int K) {
+  const size_t elem = dt == S2V_F32 ? 4 : 8, G = 32 / elem;
+  return (size_t)sh->batch * sh->num_rows * ((K + G - 1) / G) * G * elem;
+}
+
+int s2v_theta2_einsum(s2v_dtype dt, const s2v_shard *sh, int K, const void *t2c, void *tot,
+                      double *out, void *stream) {
+  if (K < 1) return fail(S2V_EINVAL, "embed_dim %d", K);
+  cudaStream_t st = as_stream(stream);
+  const size_t elem = dt == S2V_F32 ? 4 : 8, G = 32 / elem;
+  const int ng = (int)((K + G - 1) / G);
+  const int grid = sh->batch * ng;
+  const size_t smem = (size_t)kEinStages * kEinRows * 32;
+  if (dt == S2V_F32) {
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(theta2_einsum_kernel<float>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    theta2_einsum_kernel<float><<<grid, 256, smem, st>>>((const float *)t2c, sh->num_rows, K,
+                                                         (float *)tot);
+    S2V_LAUNCH_CHECK();
+    theta2_finish_kernel<float><<<1, 128, 0, st>>>((const float *)tot, sh->batch, K, out);
+  } else {
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(theta2_einsum_kernel<double>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    theta2_einsum_kernel<double><<<grid, 256, smem, st>>>((const double *)t2c, sh->num_rows, K,
+                                                          (double *)tot);
+    S2V_LAUNCH_CHECK();
+    theta2_finish_kernel<double><<<1, 128, 0, st>>>((const double *)tot, sh->batch, K, out);
   }
   S2V_LAUNCH_CHECK();
   return S2V_OK;

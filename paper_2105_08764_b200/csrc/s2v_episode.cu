@@ -61,23 +61,30 @@ __global__ void select_kernel(int B, int dmax, int64_t N, Schedule sched,
                               const uint64_t *__restrict__ keys, const uint8_t *__restrict__ active,
                               int64_t *__restrict__ picks, int32_t *__restrict__ evaluated,
                               int32_t *__restrict__ error) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+  // one block: an active slot with no candidates raises the reference's
+  // InvalidActionError("empty candidate set") BEFORE any apply
+  // (inference.py:119-122), so then no slot gets a pick this evaluation
+  __shared__ int s_err;
+  if (threadIdx.x == 0) s_err = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x)
+    if (active[b] && counts[b] == 0) s_err = 1;
+  __syncthreads();
+  const bool err = s_err != 0;
+  if (err && threadIdx.x == 0) *error = 1;  // sticky: the host zeroes it per call / chunk
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
     int d = 0;
-    if (active[b]) {
+    if (active[b] && !err) {
       const int64_t c = counts[b];
-      if (c == 0) {
-        *error = 1;  // InvalidActionError("empty candidate set")
-      } else {
-        d = sched.fallback;
-        for (int i = 0; i < sched.n; i++)
-          if ((double)c > sched.frac[i] * (double)N) {
-            d = sched.d[i];
-            break;
-          }
-        if ((int64_t)d > c) d = (int)c;
-      }
+      d = sched.fallback;
+      for (int i = 0; i < sched.n; i++)
+        if ((double)c > sched.frac[i] * (double)N) {
+          d = sched.d[i];
+          break;
+        }
+      if ((int64_t)d > c) d = (int)c;
     }
-    evaluated[b] = active[b] ? 1 : 0;
+    evaluated[b] = active[b] && !err ? 1 : 0;
     for (int j = 0; j < dmax; j++)
       picks[(int64_t)b * dmax + j] =
           j < d ? (int64_t)(~keys[((int64_t)b * dmax + j) * 2 + 1]) : (int64_t)-1;

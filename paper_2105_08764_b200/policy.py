@@ -231,7 +231,15 @@ def _peer_list(state: PartitionedState, dc, name: str, t: torch.Tensor, as_array
     (a collective on every rank at the same point)."""
     if not getattr(dc, "supports_push", False):
         return None
-    key = (t.data_ptr(), t.numel(), as_array)
+    # key by a registration generation stamped on the tensor object, not by
+    # its address: every rank (re)allocates its workspaces at the same
+    # points, so the generations agree across ranks, while a reused address
+    # on one rank only would desynchronise the peers_of collective
+    gen = getattr(t, "_s2v_peer_gen", None)
+    if gen is None:
+        gen = state._peer_gen = getattr(state, "_peer_gen", 0) + 1
+        t._s2v_peer_gen = gen
+    key = (gen, t.numel(), as_array)
     return state.workspace(f"peers:{name}", key,
                            lambda: dc.peer_array(t) if as_array else dc.peers_of(t))
 
@@ -661,12 +669,15 @@ def _loss_pack(state: PartitionedState, actions: np.ndarray, targets: np.ndarray
         "dm": torch.zeros(full, dtype=tdt, device=dev),
         "p4": torch.empty(nblk * k * k, dtype=tdt, device=dev),
         "pp": torch.empty(nblk * plen, dtype=tdt, device=dev),
+        "t2tot": torch.empty(b * k, dtype=tdt, device=dev),
         "pack": torch.empty(4 * k * k + 4 * k + 1, dtype=torch.float64, device=dev)})
     ws["actions"].copy_(torch.from_numpy(actions))
     ws["targets"].copy_(torch.from_numpy(np.ascontiguousarray(targets)))
     # g = pairwise sum of h_L (policy.py:199-200), kept on device
     emb = DeviceEmbedding(state, hs[-1], k, dtype, gathered=True)
-    wsb = lib.s2v_colsum_workspace(state.shard_ref(), k, dtype.itemsize)
+    # the "colsum" workspace is shared with _colsum_device: sized for both
+    wsb = max(lib.s2v_colsum_workspace(state.shard_ref(), k, dtype.itemsize),
+              lib.s2v_colsum_residual_workspace(state.shard_ref(), k, dtype.itemsize))
     cs = state.workspace("colsum", (k, dtype.str), lambda: {
         "ws": torch.empty(max(wsb // dtype.itemsize, 1), dtype=tdt, device=dev),
         "g": torch.empty(b * k, dtype=tdt, device=dev)})
@@ -692,11 +703,21 @@ def _loss_pack(state: PartitionedState, actions: np.ndarray, targets: np.ndarray
             break
         _allgather_rows(state, comm, ws["dm"], k, "embed_bwd", name="dm")
         _lib.call("s2v_gather", dt, state.shard_ref(), k, ptr(ws["dm"]), ptr(ws["grad_h"]), s)
+    # dtheta2's einsum terms go to a chain-layout buffer: grad_h is free by
+    # now and has the size unless K is not a multiple of 32 / itemsize
+    t2b = lib.s2v_theta2_terms_bytes(dt, state.shard_ref(), k)
+    t2c = ws["grad_h"] if t2b <= ws["grad_h"].numel() * dtype.itemsize else \
+        state.workspace("theta2_terms", (t2b,), lambda: torch.empty(
+            t2b // dtype.itemsize, dtype=tdt, device=dev))
     _lib.call("s2v_param_grads", dt, state.shard_ref(), k, dparams.ptr("theta2"),
-              dparams.ptr("theta3"), ptr(ws["dzsum"]), ptr(ws["pp"]), s)
+              dparams.ptr("theta3"), ptr(ws["dzsum"]), ptr(ws["pp"]), ptr(t2c), s)
     pack = ws["pack"]
     base = pack.data_ptr()
     _lib.call("s2v_reduce_partials", dt, ptr(ws["pp"]), nblk, plen, base, s)  # t1, t2, t3
+    # dtheta2 in the reference's einsum order (policy.py:305-306) replaces
+    # the partial-sum value: the 4M-term sum cancels heavily at BA(2M,16)
+    _lib.call("s2v_theta2_einsum", dt, state.shard_ref(), k, ptr(t2c), ptr(ws["t2tot"]),
+              base + 8 * k, s)
     _lib.call("s2v_reduce_partials", dt, ptr(ws["p4"]), nblk, k * k, base + 8 * plen, s)
     _lib.call("s2v_reduce_partials", _lib.S2V_F64, ptr(ws["head"]), b, head_len,
               base + 8 * (plen + k * k), s)  # t5, t6, t7, sq_err

@@ -16,8 +16,13 @@ GOLD = Path(__file__).resolve().parent / "golden"
 
 
 @pytest.mark.parametrize("name,tol", [("train_ba1000_b4_k64_l5", 1e-4),
-                                      ("train_ba600_b3_k16_l3_f64", 1e-9)])
+                                      ("train_ba600_b3_k16_l3_f64", 1e-9),
+                                      ("train_cfg2_ba10k_b32_k64_l5", 1e-4)])
 def test_training_step_matches_reference(name, tol):
+    """Reference training steps (oracle/make_golden.py).  train_cfg2_* is
+    BASELINE configs[1] itself: 32 x BA(10000,4,100+i), B = 32, tau = 4; at
+    B = 32 the Bellman targets go through the device u1's sequential-sgemm
+    branch (csrc/s2v_episode.cu), which they pin bitwise."""
     path = GOLD / f"{name}.npz"
     if not path.exists():
         pytest.skip("golden fixture not generated")
@@ -48,6 +53,37 @@ def test_training_step_matches_reference(name, tol):
     for k in P.PARAM_NAMES:
         assert scale_error(g0[k], z[f"g0_{k}"]).max() < tol, k
         assert scale_error(getattr(params, k), z[f"p1_{k}"]).max() < tol, k
+
+
+def test_cfg2_device_tau_loop_matches_reference():
+    """BASELINE configs[1] through train_step's device-resident tau loop
+    (policy.train_iterations): per-iteration losses and the post-Adam
+    parameters and moments after tau = 4 match the reference's at 1e-4."""
+    from paper_2105_08764_b200.policy import train_iterations
+    path = GOLD / "train_cfg2_ba10k_b32_k64_l5.npz"
+    if not path.exists():
+        pytest.skip("golden fixture not generated")
+    z = np.load(path)
+    n, m, B, K, L, tau = (int(z[k]) for k in ("n", "m", "B", "K", "L", "tau"))
+    dataset = [P.generate_ba(n, m, 100 + i) for i in range(B)]
+    params = P.PolicyParams(num_layers=L, **{k: z[f"p0_{k}"].copy() for k in P.PARAM_NAMES})
+    batch = [P.ExperienceTuple(i, P.pack_solution(z["snaps"][i]), int(z["actions"][i]), 0.0)
+             for i in range(B)]
+
+    def worker(comm):
+        part = P.partition_rows(n, 1)[0]
+        adam = P.AdamState.create(params, lr=1e-5)
+        state = P.tuples_to_graphs(batch, dataset, part)
+        targets = P.batch_targets(batch, dataset, params, comm, part, 0.9).astype(np.float32)
+        losses = train_iterations(state, z["actions"], targets, params, adam, tau, comm)
+        return targets, losses, adam
+    targets, losses, adam = P.run_workers(1, worker)[0]
+    assert np.array_equal(targets, z["targets"])
+    assert scale_error(losses, z["losses"]).max() < 1e-4
+    for k in P.PARAM_NAMES:
+        assert scale_error(getattr(params, k), z[f"p1_{k}"]).max() < 1e-4, k
+        assert scale_error(adam.m[k], z[f"m_{k}"]).max() < 1e-4, k
+        assert scale_error(adam.v[k], z[f"v_{k}"]).max() < 1e-4, k
 
 
 @pytest.mark.parametrize("dtype,tol", [(np.float32, 1e-4), (np.float64, 1e-9)])
@@ -192,3 +228,38 @@ def test_device_tau_loop_rejects_non_finite():
         return msg, same, adam.step
     msg, same, step = P.run_workers(1, worker)[0]
     assert "non-finite gradient" in msg and same and step == 0
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("B,n,K", [(1, 5, 8), (2, 1003, 64), (3, 4099, 16), (2, 70001, 64),
+                                   (1, 2049, 2)])
+def test_theta2_einsum_order_bitwise(dtype, B, n, K):
+    """s2v_theta2_einsum reproduces np.einsum("bkv,bv->k") (policy.py:305-306)
+    bit for bit on terms with heavy cancellation, tails included: with
+    deg = 1 the einsum's products are the terms themselves."""
+    import torch
+    from paper_2105_08764_b200 import _lib
+    from paper_2105_08764_b200.device import stream_ptr
+    rng = np.random.default_rng(B * n + K)
+    X = (rng.normal(size=(B, K, n)) * np.exp(rng.normal(size=(B, K, n)) * 4)).astype(dtype)
+    want = np.einsum("bkv,bv->k", X, np.ones((B, n), dtype))
+    G = 32 // np.dtype(dtype).itemsize
+    ng = (K + G - 1) // G
+    lay = np.zeros((B, ng * G, n), dtype)
+    lay[:, :K] = X
+    lay = np.ascontiguousarray(lay.reshape(B, ng, G, n).transpose(0, 1, 3, 2))
+    g = P.Graph(n, [(i, i + 1) for i in range(n - 1)])
+
+    def worker(comm):
+        st = P.PartitionedState([g] * B, P.partition_rows(n, 1)[0], dtype=dtype)
+        lib = _lib.load()
+        dt = _lib.S2V_F32 if dtype == np.float32 else _lib.S2V_F64
+        assert lib.s2v_theta2_terms_bytes(dt, st.shard_ref(), K) == lay.nbytes
+        t2c = torch.from_numpy(lay.ravel()).to(st.device)
+        tot = torch.empty(B * K, dtype=t2c.dtype, device=st.device)
+        out = torch.empty(K, dtype=torch.float64, device=st.device)
+        _lib.call("s2v_theta2_einsum", dt, st.shard_ref(), K, t2c.data_ptr(), tot.data_ptr(),
+                  out.data_ptr(), stream_ptr())
+        return out.cpu().numpy()
+    got = P.run_workers(1, worker)[0]
+    assert np.array_equal(got.astype(dtype), want)
