@@ -131,3 +131,26 @@ def forward(row_ptr, cols, sol, theta: dict, num_layers: int, dtype=np.float32):
     cand = ((deg > 0) & (np.asarray(sol) == 0)).astype(np.uint8)
     sc = scores(h, cand, theta, u1)
     return h, g, u1, cand, sc
+
+
+def generate_ba_edges(n: int, d: int, seed: int) -> np.ndarray:
+    """graphrl.generate_ba(n, d, seed).edge_array via the C restatement
+    (ba_oracle.c, graphs.py:125-157); used by bench.py's reference arm to
+    build its input graph without the product library."""
+    build()
+    L = ctypes.CDLL(str(HERE / "libba_oracle.so"))
+    L.s2vo_generate_ba.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                   ctypes.c_void_p]
+    L.s2vo_generate_ba.restype = ctypes.c_int64
+    st = np.random.default_rng(seed).bit_generator.state
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    m = (1 << 64) - 1
+    words = np.array([s >> 64, s & m, inc >> 64, inc & m, int(st["has_uint32"]),
+                      int(st["uinteger"])], dtype=np.uint64)
+    num = L.s2vo_generate_ba(n, d, words.ctypes.data, None)
+    if num < 0:
+        raise ValueError(f"generate_ba({n}, {d}) out of range")
+    edges = np.empty((num, 2), dtype=np.int64)
+    if L.s2vo_generate_ba(n, d, words.ctypes.data, edges.ctypes.data) != num:
+        raise RuntimeError("oracle BA generator failed")
+    return edges

@@ -165,3 +165,14 @@ def test_native_rmat_equals_numpy_definition(scale, chunk):
     b = P.graphs.generate_rmat_numpy(scale, 16, 0, chunk=chunk)
     assert a.num_nodes == b.num_nodes
     assert np.array_equal(a.edge_array, b.edge_array)
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_oracle_ba_generator_equals_reference_bytes(case):
+    """The C restatement that builds the reference arm's input graph
+    (oracle/ba_oracle.c) == the reference's generate_ba, byte for byte."""
+    import hashlib
+    gold = json.loads((GOLD / "generators.json").read_text())["ba"][case]
+    e = cref.generate_ba_edges(gold["n"], gold["d"], gold["seed"])
+    assert e.shape[0] == gold["edges"]
+    assert hashlib.sha256(np.ascontiguousarray(e).tobytes()).hexdigest() == gold["sha256"]
