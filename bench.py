@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--nodes", type=int, default=2_000_000)
     ap.add_argument("--m", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-steps", type=int, default=3,
+                    help="reference arm: full steps actually run (>= 3, min reported)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--train-steps", type=int, default=5)
@@ -185,64 +187,170 @@ def peaks():
 # ---------------------------------------------------------------------------
 
 
-def cpu_state(graph):
-    from oracle import port
-    t0 = time.perf_counter()
-    st = port.ResidualState([graph.edge_array], graph.num_nodes, dtype=np.float32)
-    return st, time.perf_counter() - t0
+def reference_module():
+    """The unmodified reference package graphrl, pip-installed from
+    /root/reference into baseline/_ref (git-ignored; travels to the box).
+    Returns (module, kind, description); falls back to oracle/port.py (the
+    reference's numpy/scipy calls restated) when the install is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "graphrl" / "__init__.py").exists():
+        if str(ref) not in sys.path:
+            sys.path.insert(0, str(ref))
+        import graphrl
+        return graphrl, "reference", ("graphrl 0.1.0 (pip install --target baseline/_ref "
+                                      "/root/reference), its own public API")
+    return None, "port", "oracle/port.py (reference numpy/scipy calls restated)"
 
 
-def cpu_sample(st, theta, layers=5):
-    """One bounded sample of the reference algorithm's inference step on the
-    same graph: one full embedding round (spmm + theta4 + relu) timed, times
-    the 5 rounds of a step, plus q_forward + masked select + group apply.
-    Returns (estimated step seconds, detail)."""
-    from oracle import port
-    t0 = time.perf_counter()
-    h1 = port.embed(st, theta, 1)
-    t_round = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    s = port.scores(h1, st.cand, theta)
-    gl = port.masked(s, st.cand)
+def _libs2v_mapped() -> bool:
+    """Whether this process mapped the product library (must be False for
+    the reference arm)."""
+    try:
+        return "libs2v.so" in Path("/proc/self/maps").read_text()
+    except Exception:
+        return False
+
+
+def host_info():
+    """CPU model, logical cores and the BLAS pool the reference's numpy uses."""
+    model = ""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{k: d.get(k) for k in ("internal_api", "num_threads", "version", "architecture")}
+                for d in threadpool_info() if d.get("user_api") == "blas"]
+    except Exception:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "blas": blas,
+            "scipy_spmm_threads": 1}
+
+
+def ref_inference_step(R, st, params, comm, sched, n):
+    """One iteration of the reference's solve loop (inference.py:107-147)
+    through its public API: embed_forward, q_forward, masked_scores, the
+    select all-gather, d_for + select_top_d, group apply with the mid-group
+    skip, residual_counts."""
+    emb = R.embed_forward(st, params, comm)
+    sc = R.q_forward(emb, st.cand, params, comm)
+    gl = comm.all_gather(R.masked_scores(sc, st.cand), axis=-1, tag="select")
     cm = np.isfinite(gl[0])
-    picks = port.select_top_d(gl[0], cm, port.d_for(int(cm.sum()), st.n))
+    picks = R.select_top_d(gl[0], cm, sched.d_for(int(np.count_nonzero(cm)), n))
     for j, v in enumerate(picks):
         if j > 0 and not st.cand[0, v]:
             continue
-        st.apply(v, 0)
-    t_rest = time.perf_counter() - t0
-    est = layers * t_round + t_rest
-    return est, {"round_s": round(t_round, 3), "q_select_apply_s": round(t_rest, 3)}
+        st.apply_action(v, slot=0)
+    return st.residual_counts(comm)
+
+
+def ref_graph(R, nodes, m):
+    """The reference's Graph of generate_ba(nodes, m, 0), built from the
+    edge array of the oracle's C restatement of generate_ba (pinned byte for
+    byte against the reference; the reference's own Python loop takes
+    216 s at 2M nodes).  The product library libs2v.so is never loaded."""
+    from oracle import cref
+    edges = cref.generate_ba_edges(nodes, m, 0)
+    if R is None:
+        return edges
+    return R.Graph(nodes, edges)
+
+
+def port_params(K, L, seed):
+    """PolicyParams.initialize(K, L, seed) (policy.py:79-102) without the
+    product package: one default_rng(seed) stream, theta1..theta7 in order,
+    U(-0.05, 0.05) fp32, |theta6| and |theta7[K:]| ("positive")."""
+    rng = np.random.default_rng(seed)
+    shapes = [(K, 1), (K, 1), (K, K), (K, K), (K, K), (K, K), (2 * K, 1)]
+    th = {f"theta{i + 1}": rng.uniform(-0.05, 0.05, size=sh).astype(np.float32)
+          for i, sh in enumerate(shapes)}
+    th["theta6"] = np.abs(th["theta6"])
+    th["theta7"][K:] = np.abs(th["theta7"][K:])
+    return th
+
+
+def cpu_baseline_infer(graph):
+    """cpu_baseline of the headline: ONE full inference step of the reference
+    (from S = {}) on the same graph, this host's cores."""
+    R, kind, desc = reference_module()
+    if R is None:
+        from oracle import port
+        st = port.ResidualState([graph.edge_array], graph.num_nodes)
+        t0 = time.perf_counter()
+        port.inference_step(st, port_params(64, 5, 0), 5, np.array([True]))
+        dt = time.perf_counter() - t0
+    else:
+        g = R.Graph(graph.num_nodes, graph.edge_array)
+        params = R.PolicyParams.initialize(64, 5, seed=0)
+        comm = R.WorkerGroup(1).comm(0)
+        st = R.PartitionedState([g], R.partition_rows(graph.num_nodes, 1)[0])
+        t0 = time.perf_counter()
+        ref_inference_step(R, st, params, comm, R.SelectionSchedule.adaptive(), graph.num_nodes)
+        dt = time.perf_counter() - t0
+    return {"value": dt, "unit": "s", "cores": os.cpu_count(), "kind": kind,
+            "sample": f"{desc}: one full inference step (5 rounds + q + select + apply) from "
+                      f"S = {{}} on the same graph", "host": host_info()}
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU inference step, timed on
+    this host, rank 0 only.  Each step is one full policy evaluation +
+    selection + apply of the episode from S = {}; min over the steps that
+    actually ran (at least 3)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2105_08764_b200.graphs as G
-    from paper_2105_08764_b200.policy import PolicyParams
-    graph = G.generate_ba(args.nodes, args.m, 0)
-    theta = PolicyParams.initialize(64, 5, seed=0).as_dict()
-    cores = os.cpu_count()
-    st, build = cpu_state(graph)
-    for _ in range(args.warmup):
-        cpu_sample(st, theta)
-    vals, detail = [], None
-    for _ in range(args.steps):
-        v, detail = cpu_sample(st, theta)
-        vals.append(v)
-    value = float(np.mean(vals))
-    sample = ("reference algorithm (oracle/port.py, numpy/scipy restatement of graphrl) "
-              "on the same graph: per step, 1 timed embedding round x 5 + q_forward + "
-              f"select + apply; {detail}; state build {build:.1f}s excluded")
+    R, kind, desc = reference_module()
+    t0 = time.perf_counter()
+    g = ref_graph(R, args.nodes, args.m)
+    t_graph = time.perf_counter() - t0
+    nsteps = max(3, args.ref_steps)
+    if R is not None:
+        params = R.PolicyParams.initialize(64, 5, seed=0)
+        comm = R.WorkerGroup(1).comm(0)
+        t0 = time.perf_counter()
+        st = R.PartitionedState([g], R.partition_rows(args.nodes, 1)[0])
+        t_build = time.perf_counter() - t0
+        sched = R.SelectionSchedule.adaptive()
+        times = []
+        for _ in range(nsteps):
+            t0 = time.perf_counter()
+            ref_inference_step(R, st, params, comm, sched, args.nodes)
+            times.append(time.perf_counter() - t0)
+    else:  # port fallback: the same loop body, restated (oracle/port.py)
+        from oracle import port
+        theta = port_params(64, 5, 0)
+        t0 = time.perf_counter()
+        st = port.ResidualState([g], args.nodes)
+        t_build = time.perf_counter() - t0
+        times = []
+        for _ in range(nsteps):
+            t0 = time.perf_counter()
+            port.inference_step(st, theta, 5, np.array([True]))
+            times.append(time.perf_counter() - t0)
+    value = float(min(times))
+    info = host_info()
+    sample = (f"{desc}: {nsteps} full inference steps (embed_forward 5 rounds + q_forward + "
+              f"select all-gather + top-d + group apply + residual_counts) of the adaptive "
+              f"episode from S = {{}}, min over steps; step times "
+              f"{[round(t, 2) for t in times]} s; graph {t_graph:.1f}s and PartitionedState "
+              f"build {t_build:.1f}s excluded")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": args.gpus, "steps": nsteps, "warmup": 0,
             "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload(args),
-            "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "port",
-                             "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "s", "cores": os.cpu_count(), "kind": kind,
+                             "sample": sample, "host": info},
             "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "step_times_s": times, "mean_step_s": float(np.mean(times)),
+            "product_library_mapped": _libs2v_mapped(),
+            "setup": {"graph_s": round(t_graph, 2), "state_build_s": round(t_build, 2)}}
     print(json.dumps(line), flush=True)
 
 
@@ -295,32 +403,73 @@ def train_leg(P, comm, dataset, B, tau, steps, warmup, name):
             "path": "train_step(buffer, dataset, params, adam, cfg, rng, comm, part)"}
 
 
-def cpu_train_sample(dataset, B_sample, B, tau):
-    """Reference algorithm (oracle/port.py) training step on B_sample of the B
-    tuples, scaled by B / B_sample (the step is linear in B)."""
-    from oracle import port
-    import paper_2105_08764_b200 as P
-    n = dataset[0].num_nodes
+def cpu_baseline_train(P, dataset, B, tau):
+    """BASELINE configs[1] on the CPU: ONE full train_step of the reference
+    (tuples_to_graphs + batch_targets + tau x (loss_and_gradients +
+    adam_step)) on the same B tuples, this host's cores."""
+    R, kind, desc = reference_module()
     buf = _train_buffer(P, dataset, B)
-    tuples = [buf[i] for i in range(B_sample)]
-    theta = P.PolicyParams.initialize(64, 5, seed=0).as_dict()
-    edges = [dataset[t.graph_index].edge_array for t in tuples]
-    snaps = np.stack([P.unpack_solution(t.solution_snapshot, n) for t in tuples])
-    acts = np.array([t.action for t in tuples])
+    if R is None:
+        return None
+    graphs = [R.Graph(g.num_nodes, g.edge_array) for g in dataset]
+    rbuf = R.ReplayBuffer(max(B, 1))
+    for i in range(len(buf)):
+        t = buf[i]
+        rbuf.add(R.ExperienceTuple(t.graph_index, t.solution_snapshot, t.action, 0.0))
+    params = R.PolicyParams.initialize(64, 5, seed=0)
+    adam = R.AdamState.create(params, lr=1e-5)
+    cfg = R.TrainConfig(embed_dim=64, num_layers=5, batch_size=B, tau=tau)
+    comm = R.WorkerGroup(1).comm(0)
+    part = R.partition_rows(dataset[0].num_nodes, 1)[0]
     t0 = time.perf_counter()
-    st = port.ResidualState(edges, n, solutions=snaps)
-    tg = port.batch_targets(edges, n, snaps, acts, theta, 5, 0.9).astype(np.float32)
-    m = {k: np.zeros_like(v) for k, v in theta.items()}
-    v = {k: np.zeros_like(x) for k, x in theta.items()}
-    step = 0
-    for _ in range(tau):
-        _, grads = port.loss_and_grads(st, acts, tg, theta, 5)
-        step = port.adam(theta, grads, m, v, step, 1e-5)
+    R.train_step(rbuf, graphs, params, adam, cfg, np.random.default_rng(7), comm, part)
     dt = time.perf_counter() - t0
-    return {"value": dt * B / B_sample, "unit": "s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"oracle/port.py train step on {B_sample} of {B} tuples (tuples_to_graphs + "
-                      f"batch_targets + {tau} x (loss_and_grads + adam)) = {dt:.2f}s, "
-                      f"scaled x{B / B_sample:g}"}
+    return {"value": dt, "unit": "s", "cores": os.cpu_count(), "kind": kind,
+            "sample": f"{desc}: one full train_step (B={B}, tau={tau}) on the same tuples"}
+
+
+def cpu_baseline_cfg4(graph, B, tau, L=5, K=64):
+    """BASELINE configs[3] on the CPU, bounded sample (the full step is
+    ~10^3-10^4 s): on one tuple of the same graph, time the reference's
+    PartitionedState build, one embedding round (policy.py:163-174:
+    state.spmm + theta4 matmul + relu) and one backward layer
+    (policy.py:290-304: the three einsums, two matmuls, state.spmm_t), then
+    scale to train_step's B x (state build x 2 + L forward rounds for the
+    targets) + tau x B x L x (forward round + backward layer)."""
+    R, kind, desc = reference_module()
+    if R is None:
+        return None
+    n = graph.num_nodes
+    g = R.Graph(n, graph.edge_array)
+    t0 = time.perf_counter()
+    st = R.PartitionedState([g], R.partition_rows(n, 1)[0])
+    t_state = time.perf_counter() - t0
+    rng = np.random.default_rng(0)
+    th = {k: v for k, v in R.PolicyParams.initialize(K, L, seed=0).as_dict().items()}
+    h = np.abs(rng.normal(size=(1, K, n))).astype(np.float32)
+    e12 = rng.normal(size=(1, K, n)).astype(np.float32)
+    t0 = time.perf_counter()
+    m = np.ascontiguousarray(st.spmm(h))
+    z = e12 + np.matmul(th["theta4"], m)
+    h2 = np.maximum(z, 0)
+    t_fwd = time.perf_counter() - t0
+    w = np.abs(rng.normal(size=(1, K, n))).astype(np.float32)
+    sol = np.zeros((1, n), np.float32)
+    t0 = time.perf_counter()
+    dz = h2 * (z > 0)
+    np.einsum("bkv,bv->k", dz, sol)
+    np.einsum("bkv,bjv->kj", dz, w)
+    np.matmul(th["theta3"].T, dz)
+    np.einsum("bkv,bjv->kj", dz, m)
+    st.spmm_t(np.matmul(th["theta4"].T, dz))
+    t_bwd = time.perf_counter() - t0
+    est = B * (2 * t_state + L * t_fwd) + tau * B * L * (t_fwd + t_bwd)
+    return {"value": est, "unit": "s", "cores": os.cpu_count(), "kind": kind,
+            "sample": f"{desc} building blocks on 1 tuple of the same graph: PartitionedState "
+                      f"{t_state:.2f}s, forward round {t_fwd:.2f}s, backward layer {t_bwd:.2f}s;"
+                      f" scaled as B*(2*state + L*fwd) + tau*B*L*(fwd + bwd), B={B}, "
+                      f"tau={tau}, L={L} (an estimate: the measured full reference step at "
+                      "B=2, tau=1 is 531 s, SURVEY.md section 6)"}
 
 
 # ---------------------------------------------------------------------------
@@ -521,12 +670,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cst, build = cpu_state(graph)
-        est, detail = cpu_sample(cst, params.as_dict())
-        detail["state_build_s"] = round(build, 2)
-        cpu = {"value": est, "unit": "s", "cores": os.cpu_count(), "kind": "port",
-               "sample": "oracle/port.py (reference numpy/scipy algorithm) on the same graph: "
-                         f"1 timed embedding round x 5 + q + select + apply; {detail}"}
+        cpu = cpu_baseline_infer(graph)
 
     train = None
     if not args.no_train:
@@ -536,11 +680,13 @@ def main():
                          "MVC DQN training step, 32 x BA(10000,4,seed=100+i), K=64, T=5, tau=4 "
                          "(BASELINE configs[1])")
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            leg2["cpu_baseline"] = cpu_train_sample(ds2, 4, 32, 4)
+            leg2["cpu_baseline"] = cpu_baseline_train(P, ds2, 32, 4)
         train.append(leg2)
         leg4 = train_leg(P, comm, [graph], 8, 4, max(2, args.train_steps // 2), 2,
                          f"MVC DQN training step, 8 tuples of BA({args.nodes},{args.m},0) "
                          "(node-level batch), K=64, T=5, tau=4 (BASELINE configs[3])")
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            leg4["cpu_baseline"] = cpu_baseline_cfg4(graph, 8, 4)
         train.append(leg4)
 
     extra = None
@@ -554,15 +700,25 @@ def main():
         leg1["full_solve_cover"] = res.cover_size
         leg1["full_solve_evals"] = res.policy_evals
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            from oracle import port
-            theta = P.PolicyParams.initialize(64, 5, seed=0).as_dict()
-            t0 = time.perf_counter()
-            (cover, evals, _, _), = port.solve([g1.edge_array], 1000, theta, 5)
-            dt = time.perf_counter() - t0
+            R, kind, desc = reference_module()
+            if R is not None:
+                rg = R.Graph(1000, g1.edge_array)
+                rp = R.PolicyParams.initialize(64, 5, seed=0)
+                t0 = time.perf_counter()
+                (rr,) = R.run_workers(1, lambda c: R.solve([rg], rp, c))[0]
+                dt = time.perf_counter() - t0
+                cover_n, evals = rr.cover_size, rr.policy_evals
+            else:
+                from oracle import port
+                t0 = time.perf_counter()
+                (cover, evals, _, _), = port.solve([g1.edge_array], 1000, port_params(64, 5, 0),
+                                                   5)
+                dt = time.perf_counter() - t0
+                cover_n = len(cover)
             leg1["cpu_baseline"] = {"value": dt / evals, "unit": "s", "cores": os.cpu_count(),
-                                    "kind": "port", "full_adaptive_solve_s": dt,
-                                    "sample": f"oracle/port.py full adaptive solve ({evals} evals,"
-                                              f" cover {len(cover)}) / evals"}
+                                    "kind": kind, "full_adaptive_solve_s": dt,
+                                    "sample": f"{desc}: full adaptive solve ({evals} evals, "
+                                              f"cover {cover_n}) / evals"}
         extra.append(leg1)
         t0 = time.time()
         g5 = P.generate_rmat(args.rmat_scale, 16, 0)
