@@ -153,7 +153,98 @@ def generator_fixture(R):
     (OUT / "generators.json").write_text(json.dumps(out, indent=1))
 
 
+ALG5 = dict(n=400, m=4, graphs=4, seed0=200, K=64, L=3, B=4, tau=2, lr=1e-3, eps_start=1.0,
+            eps_end=0.0, eps_decay=12, capacity=64, cfg_seed=5, eval_every=10, steps=40,
+            resume_at=20, eval_n=400, eval_seed=999, ref_size=200)
+
+
+def alg5_fixture(R):
+    """Algorithm 5 end to end: the reference's train() (agent.py:273-348)
+    for ALG5["steps"] steps on a BA dataset, with every act / compute_target
+    / train_step result recorded (hooks on the agent module), plus the same
+    run split in two with the checkpoint + train_state.npz resume of
+    cli.py:152-178 (params via save/load_checkpoint, Adam m/v/step/lr and
+    global_step via np.savez)."""
+    import tempfile
+    import graphrl.agent as ag
+    c = ALG5
+    dataset = [R.generate_ba(c["n"], c["m"], c["seed0"] + i) for i in range(c["graphs"])]
+    evals = [R.generate_ba(c["eval_n"], c["m"], c["eval_seed"])]
+    cfg = ag.TrainConfig(embed_dim=c["K"], num_layers=c["L"], batch_size=c["B"], tau=c["tau"],
+                         learning_rate=c["lr"], replay_capacity=c["capacity"],
+                         eps_start=c["eps_start"], eps_end=c["eps_end"],
+                         eps_decay_steps=c["eps_decay"], eval_every=c["eval_every"],
+                         seed=c["cfg_seed"])
+    log = {"act": [], "target": [], "loss": []}
+    o_act, o_tgt, o_ts = ag.act, ag.compute_target, ag.train_step
+
+    def h_act(*a, **k):
+        v = o_act(*a, **k)
+        log["act"].append(int(v))
+        return v
+
+    def h_tgt(*a, **k):
+        t = o_tgt(*a, **k)
+        log["target"].append(float(t))
+        return t
+
+    def h_ts(*a, **k):
+        ls = o_ts(*a, **k)
+        log["loss"].append([float(x) for x in ls])
+        return ls
+    ag.act, ag.compute_target, ag.train_step = h_act, h_tgt, h_ts
+    out = {}
+    try:
+        def run(tag, **kw):
+            for key in log:
+                log[key] = []
+            probe = {}
+            params, metrics = R.run_workers(1, lambda comm: ag.train(
+                dataset, cfg, comm, eval_graphs=evals, reference_sizes=[c["ref_size"]],
+                probe=probe, **kw))[0]
+            out[f"{tag}_act"] = np.array(log["act"], np.int64)
+            out[f"{tag}_target"] = np.array(log["target"], np.float64)
+            flat = [x for ls in log["loss"] for x in ls]
+            out[f"{tag}_loss"] = np.array(flat, np.float64)
+            out[f"{tag}_loss_len"] = np.array([len(ls) for ls in log["loss"]], np.int64)
+            out[f"{tag}_metrics"] = np.array([[r.step, r.epsilon, r.loss, r.mean_approx_ratio,
+                                               r.cover_size_mean] for r in metrics], np.float64)
+            adam = probe["adam_state"]
+            for k, v in params.as_dict().items():
+                out[f"{tag}_p_{k}"] = v
+                out[f"{tag}_m_{k}"] = adam.m[k]
+                out[f"{tag}_v_{k}"] = adam.v[k]
+            out[f"{tag}_adam_step"] = np.array(adam.step)
+            out[f"{tag}_global_step"] = np.array(probe["global_step"])
+            return params, adam, probe
+        run("full", max_steps=c["steps"])
+        params, adam, probe = run("first", max_steps=c["resume_at"])
+        with tempfile.TemporaryDirectory() as d:   # cli.py:152-178 round trip
+            R.save_checkpoint(params, Path(d) / "checkpoint.bin")
+            arrays = {"global_step": probe["global_step"], "adam_step": adam.step, "lr": adam.lr}
+            for name, arr in adam.m.items():
+                arrays[f"m_{name}"] = arr
+            for name, arr in adam.v.items():
+                arrays[f"v_{name}"] = arr
+            np.savez(Path(d) / "train_state.npz", **arrays)
+            p2 = R.load_checkpoint(Path(d) / "checkpoint.bin")
+            blob = np.load(Path(d) / "train_state.npz")
+            a2 = R.AdamState(m={k: blob[f"m_{k}"] for k in p2.as_dict()},
+                             v={k: blob[f"v_{k}"] for k in p2.as_dict()},
+                             step=int(blob["adam_step"]), lr=float(blob["lr"]))
+            run("resumed", max_steps=c["steps"] - c["resume_at"], params=p2, adam=a2,
+                start_step=int(blob["global_step"]))
+    finally:
+        ag.act, ag.compute_target, ag.train_step = o_act, o_tgt, o_ts
+    np.savez_compressed(OUT / "alg5_train_ba400_k64_l3.npz", **out)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "alg5":
+        t0 = time.time()
+        alg5_fixture(_ref())
+        print("alg5", time.time() - t0)
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "gen":
         generator_fixture(_ref())
         return

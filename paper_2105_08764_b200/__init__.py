@@ -6,13 +6,14 @@ step: the same public names and signatures, with the numerics in libs2v.so
 shards resident in HBM.  There is no CPU compute path.
 """
 from .agent import (ExperienceTuple, MetricsRow, ReplayBuffer, TrainConfig, act, batch_targets,
-                    compute_target, evaluate_ratio, pack_solution, train, train_step,
-                    tuples_to_graphs, unpack_solution)
+                    compute_target, evaluate_ratio, load_train_state, pack_solution,
+                    save_train_state, train, train_step, tuples_to_graphs, unpack_solution)
 from .collective import Comm, CollectiveStats, DistComm, WorkerGroup, run_workers
 from .env import MVC, PROBLEMS, MvcEnv, ProblemSpec, reset
 from .errors import (CollectiveAborted, CollectiveError, ConfigError, DataError, GraphRLError,
                      InvalidActionError)
-from .graphs import Graph, generate_ba, generate_er, generate_rmat, load_edge_list, write_edge_list
+from .graphs import (Graph, generate_ba, generate_er, generate_rmat, is_vertex_cover,
+                     load_edge_list, write_edge_list)
 from .inference import SelectionSchedule, SolveResult, select_top_d, solve
 from .policy import (PARAM_NAMES, AdamState, PolicyParams, adam_step, embed_forward,
                      load_checkpoint, loss_and_gradients, masked_scores, param_shapes, q_forward,

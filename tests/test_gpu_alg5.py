@@ -1,0 +1,110 @@
+"""Algorithm 5 end to end against the reference's own train()
+(pkg/src/graphrl/agent.py:273-348): every epsilon-greedy action, Bellman
+target and train_step loss of a 40-step run on a BA dataset, the eval rows,
+and the final parameters / Adam state; plus the same run split in two and
+resumed from checkpoint.bin + train_state.npz (cli.py:152-178).  Golden:
+tests/golden/alg5_train_ba400_k64_l3.npz (oracle/make_golden.py alg5).
+
+Actions and eval covers are decided by the bitwise forward (argmax, d=1
+solve) and must be identical; losses, targets and parameters carry the
+backward's 1e-4 bar."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2105_08764_b200 as P
+import paper_2105_08764_b200.agent as ag
+from reference_math import scale_error
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden" / "alg5_train_ba400_k64_l3.npz"
+C = dict(n=400, m=4, graphs=4, seed0=200, K=64, L=3, B=4, tau=2, lr=1e-3, eps_start=1.0,
+         eps_end=0.0, eps_decay=12, capacity=64, cfg_seed=5, eval_every=10, steps=40,
+         resume_at=20, eval_n=400, eval_seed=999, ref_size=200)
+
+
+@pytest.fixture(scope="module")
+def setup():
+    if not GOLD.exists():
+        pytest.skip("golden fixture not generated")
+    dataset = [P.generate_ba(C["n"], C["m"], C["seed0"] + i) for i in range(C["graphs"])]
+    evals = [P.generate_ba(C["eval_n"], C["m"], C["eval_seed"])]
+    cfg = P.TrainConfig(embed_dim=C["K"], num_layers=C["L"], batch_size=C["B"], tau=C["tau"],
+                        learning_rate=C["lr"], replay_capacity=C["capacity"],
+                        eps_start=C["eps_start"], eps_end=C["eps_end"],
+                        eps_decay_steps=C["eps_decay"], eval_every=C["eval_every"],
+                        seed=C["cfg_seed"])
+    return dataset, evals, cfg, np.load(GOLD)
+
+
+def _run(dataset, evals, cfg, **kw):
+    log = {"act": [], "target": [], "loss": []}
+    o_act, o_tgt, o_ts = ag.act, ag.compute_target, ag.train_step
+
+    def h_act(*a, **k):
+        v = o_act(*a, **k)
+        log["act"].append(int(v))
+        return v
+
+    def h_tgt(*a, **k):
+        t = o_tgt(*a, **k)
+        log["target"].append(float(t))
+        return t
+
+    def h_ts(*a, **k):
+        ls = o_ts(*a, **k)
+        log["loss"].append([float(x) for x in ls])
+        return ls
+    ag.act, ag.compute_target, ag.train_step = h_act, h_tgt, h_ts
+    try:
+        probe = {}
+        params, metrics = P.run_workers(1, lambda comm: P.train(
+            dataset, cfg, comm, eval_graphs=evals, reference_sizes=[C["ref_size"]], probe=probe,
+            **kw))[0]
+    finally:
+        ag.act, ag.compute_target, ag.train_step = o_act, o_tgt, o_ts
+    return log, params, metrics, probe
+
+
+def _check(z, tag, log, params, metrics, probe):
+    assert np.array_equal(np.array(log["act"]), z[f"{tag}_act"])
+    assert scale_error(np.array(log["target"]), z[f"{tag}_target"]).max() < 1e-4
+    assert [len(x) for x in log["loss"]] == list(z[f"{tag}_loss_len"])
+    flat = np.array([x for ls in log["loss"] for x in ls])
+    assert np.all(np.abs(flat - z[f"{tag}_loss"]) <= 1e-4 * np.abs(z[f"{tag}_loss"]))
+    got = np.array([[r.step, r.epsilon, r.loss, r.mean_approx_ratio, r.cover_size_mean]
+                    for r in metrics])
+    want = z[f"{tag}_metrics"]
+    assert got.shape == want.shape
+    assert np.array_equal(got[:, [0, 1, 3, 4]], want[:, [0, 1, 3, 4]])  # steps, eps, covers
+    assert np.all(np.abs(got[:, 2] - want[:, 2]) <= 1e-4 * np.abs(want[:, 2]))
+    adam = probe["adam_state"]
+    assert adam.step == int(z[f"{tag}_adam_step"])
+    assert probe["global_step"] == int(z[f"{tag}_global_step"])
+    for k in P.PARAM_NAMES:
+        assert scale_error(getattr(params, k), z[f"{tag}_p_{k}"]).max() < 1e-4, k
+        assert scale_error(adam.m[k], z[f"{tag}_m_{k}"]).max() < 1e-4, k
+        assert scale_error(adam.v[k], z[f"{tag}_v_{k}"]).max() < 1e-4, k
+
+
+def test_train_loop_matches_reference(setup):
+    dataset, evals, cfg, z = setup
+    _check(z, "full", *_run(dataset, evals, cfg, max_steps=C["steps"]))
+
+
+def test_train_resume_matches_reference(setup, tmp_path):
+    """20 steps, save_train_state (checkpoint.bin + train_state.npz), then
+    load_train_state and 20 more from start_step = global_step."""
+    dataset, evals, cfg, z = setup
+    log, params, metrics, probe = _run(dataset, evals, cfg, max_steps=C["resume_at"])
+    _check(z, "first", log, params, metrics, probe)
+    P.save_train_state(tmp_path, params, probe["adam_state"], probe["global_step"])
+    blob = np.load(tmp_path / "train_state.npz")
+    assert sorted(blob.files) == sorted(["global_step", "adam_step", "lr"] +
+                                        [f"{p}_{k}" for p in "mv" for k in P.PARAM_NAMES])
+    p2, a2, start = P.load_train_state(tmp_path)
+    for k in P.PARAM_NAMES:
+        assert np.array_equal(getattr(p2, k), getattr(params, k))
+    _check(z, "resumed", *_run(dataset, evals, cfg, max_steps=C["steps"] - C["resume_at"],
+                               params=p2, adam=a2, start_step=start))
