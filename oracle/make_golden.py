@@ -153,7 +153,7 @@ def generator_fixture(R):
     (OUT / "generators.json").write_text(json.dumps(out, indent=1))
 
 
-ALG5 = dict(n=400, m=4, graphs=4, seed0=200, K=64, L=3, B=4, tau=2, lr=1e-3, eps_start=1.0,
+ALG5 = dict(n=400, m=4, graphs=4, seed0=200, K=64, L=3, B=4, tau=2, lr=1e-4, eps_start=1.0,
             eps_end=0.0, eps_decay=12, capacity=64, cfg_seed=5, eval_every=10, steps=40,
             resume_at=20, eval_n=400, eval_seed=999, ref_size=200)
 
