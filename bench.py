@@ -397,10 +397,59 @@ def train_leg(P, comm, dataset, B, tau, steps, warmup, name):
         losses = P.train_step(buf, dataset, params, adam, cfg, rng, comm, part)
     e1.record()
     torch.cuda.synchronize()
-    return {"workload": name, "value": e0.elapsed_time(e1) / steps / 1e3, "unit": "s",
+    value = e0.elapsed_time(e1) / steps / 1e3
+    # roofline of the backward kernels: per-launch CUDA events over one more
+    # step (policy.BWD_TIMER), algorithmic bytes per launch from the batch
+    from paper_2105_08764_b200 import policy
+    policy.BWD_TIMER = []
+    P.train_step(buf, dataset, params, adam, cfg, rng, comm, part)
+    torch.cuda.synchronize()
+    timer, policy.BWD_TIMER = policy.BWD_TIMER, None
+    return {"workload": name, "value": value, "unit": "s",
             "B": B, "tau": tau, "steps": steps, "warmup": warmup,
             "last_losses": [float(x) for x in losses],
-            "path": "train_step(buffer, dataset, params, adam, cfg, rng, comm, part)"}
+            "path": "train_step(buffer, dataset, params, adam, cfg, rng, comm, part)",
+            "roofline": train_roofline(buf, dataset, B, part, timer)}
+
+
+def train_roofline(buf, dataset, B, part, timer):
+    """HBM roofline of the two backward kernels of loss_and_gradients at this
+    batch: spmm_t (s2v_gather, the dominant training kernel) and the
+    tcgen05 layer backward.  Bytes per launch (fp32, K = 64, rows = B x
+    local rows): gather 8(rows+1) + 4 nnz + 256 alive entries + 256 rows;
+    layer backward 256 rows x (grad_h + h_l [+ dzsum in] + dzsum out [+ m]
+    [+ dm out])."""
+    rows = B * part.num_rows
+    nnz = alive = 0
+    for i in range(min(B, len(buf))):
+        t = buf[i]
+        g = dataset[t.graph_index]
+        sol = np.unpackbits(np.frombuffer(t.solution_snapshot, np.uint8))[
+            :g.num_nodes].astype(bool)
+        e = g.edge_array
+        nnz += 2 * len(e)
+        alive += 2 * int(np.count_nonzero(~sol[e[:, 0]] & ~sol[e[:, 1]]))
+    peak, peak_src = peaks()
+    out = {"peak": peak, "peak_source": peak_src, "unit": "GB/s", "bound": "hbm"}
+    for tag, model in (("gather", lambda f: 8 * (rows + 1) + 4 * nnz + 256 * alive + 256 * rows),
+                       ("layer_backward",
+                        lambda f: 256 * rows * (2 + (0 if f[0] else 1) + 1 + int(f[1]) +
+                                                int(f[2])))):
+        ev = [(t, a, b) for t, a, b in timer if t[0] == tag]
+        if not ev:
+            continue
+        ms = [a.elapsed_time(b) for _, a, b in ev]
+        byts = [model(t[1:]) for t, _, _ in ev]
+        achieved = sum(byts) / (sum(ms) * 1e-3) / 1e9
+        out[tag] = {"achieved": round(achieved, 1), "frac": round(achieved / peak, 4),
+                    "avg_launch_ms": round(float(np.mean(ms)), 4), "launches": len(ev),
+                    "algorithmic_bytes_per_launch": int(np.mean(byts))}
+    out["kernels"] = {"gather": "gather64_tiles_kernel (spmm_t, the dominant training kernel)",
+                      "layer_backward": "layer_backward64_tc_kernel (tcgen05 split-TF32 dm and "
+                                        "dtheta4, fused dz / dzsum)"}
+    if "gather" in out:
+        out.update({"achieved": out["gather"]["achieved"], "frac": out["gather"]["frac"]})
+    return out
 
 
 def cpu_baseline_train(P, dataset, B, tau):

@@ -395,6 +395,66 @@ int s2v_merge_rank_keys(int P, int B, int d, const int64_t *gathered, int64_t *o
 int s2v_sum_ranks(int P, int64_t n, const int64_t *gathered, int64_t *out, void *stream);
 int s2v_sub_i64(int64_t *a, const int64_t *b, int n, void *stream);
 
+/* Device build of one graph's local shard structure (state.py:89-105 CSR
+ * rows, state.py:115-122 column lookup), all arrays device memory:
+ * row_ptr [rows+1] local (0-based), nbr [nnz] global neighbour ids ->
+ * cols0 [nnz] (physical rows at P > 1), col_ptr [n+1], col_ent [nnz] (stable
+ * argsort of nbr), col_row [nnz], order [rows] (stable descending-degree
+ * argsort); n_hub_out / max_deg_out: host. */
+int s2v_shard_structure(int64_t n, int P, int64_t rows_max, int64_t rows, const int64_t *row_ptr,
+                        const int32_t *nbr, int64_t nnz, int32_t *cols0, int64_t *col_ptr,
+                        int64_t *col_ent, int32_t *col_row, int32_t *order, int64_t *n_hub_out,
+                        int32_t *max_deg_out, void *stream);
+
+/* ---- handle-level API: library-owned device memory -------
+ * Plain host arrays in and out, one call per reference operation; the
+ * library allocates and owns every device buffer behind three opaque
+ * handles.  Single-rank (world = 1); P > 1 runs through the Python layer's
+ * peer-memory transports.  Same kernels, same order, same bits as the Python
+ * mirror.  theta is theta1..theta7 packed in PARAM_NAMES order with the
+ * reference's shapes (policy.py:43-113): K, K, K*K, K*K, K*K, K*K, 2K. */
+typedef struct s2v_ctx s2v_ctx;
+typedef struct s2v_graph s2v_graph;
+typedef struct s2v_state s2v_state;
+enum { S2V_OUT_EMBED = 0, S2V_OUT_SOL = 1, S2V_OUT_CAND = 2, S2V_OUT_RDEG = 3,
+       S2V_OUT_RESIDUAL = 4, S2V_OUT_SCORES = 5 };
+/* one context per GPU: run_workers' rank thread (collective.py:149-195) */
+int s2v_ctx_create(int device, int rank, int world, const void *nccl_id, s2v_ctx **out);
+int s2v_ctx_destroy(s2v_ctx *ctx);
+int s2v_ctx_sync(s2v_ctx *ctx);
+/* Graph.csr_arrays() (host row_ptr [n+1], cols [row_ptr[n]]) -> device shard
+ * structure (state.py:89-105, 115-122) */
+int s2v_graph_upload(s2v_ctx *ctx, int64_t n, const int64_t *row_ptr, const int32_t *cols,
+                     s2v_graph **out);
+int s2v_graph_destroy(s2v_graph *g);
+/* PartitionedState(graphs, part, solutions) (state.py:56-111): sol host
+ * [B][N] 0/1 bytes or NULL */
+int s2v_state_create(s2v_ctx *ctx, s2v_graph *const *graphs, int B, const uint8_t *sol,
+                     s2v_state **out);
+int s2v_state_destroy(s2v_state *st);
+int s2v_state_shard(const s2v_state *st, s2v_shard *out);
+/* embed_forward (policy.py:144-185); the embedding stays in the state */
+int s2v_embed(s2v_ctx *ctx, s2v_state *st, s2v_dtype dt, const void *theta, int K, int L);
+/* g = embed.sum(axis=2) (policy.py:199-200), host [B][K] */
+int s2v_global_sum(s2v_ctx *ctx, s2v_state *st, void *g_host);
+/* q_forward + masked_scores + top-d keys (policy.py:188-224,
+ * inference.py:61-73): keys_out host [B][d][2] {orderable score, ~node},
+ * ncand_out host [B]; d <= 8 */
+int s2v_score_topk(s2v_ctx *ctx, s2v_state *st, int d, uint64_t *keys_out, int64_t *ncand_out);
+/* one group of picks per slot with the mid-group skip rule
+ * (inference.py:125-146, state.py:173-208): picks host [B][d] (-1 padded) */
+int s2v_apply(s2v_ctx *ctx, s2v_state *st, const int64_t *picks, int d, uint8_t *applied,
+              int64_t *residual);
+/* loss_and_gradients (policy.py:232-315): grads host, packed like theta */
+int s2v_loss_grad(s2v_ctx *ctx, s2v_state *st, s2v_dtype dt, const void *theta, int K, int L,
+                  const int64_t *actions, const void *targets, void *grads, double *loss);
+/* adam_step (policy.py:339-359) in place on host arrays; step = new t */
+int s2v_adam_update(s2v_ctx *ctx, s2v_dtype dt, void *params, const void *grads, void *m,
+                    void *v, int64_t n, int step, double lr, double beta1, double beta2,
+                    double eps);
+/* host copy of a state array (S2V_OUT_*) */
+int s2v_copy_out(s2v_ctx *ctx, const s2v_state *st, int what, void *host);
+
 /* ---- graph ingestion (graphs.py:125-157) --------------------------------- */
 /* Bit-exact generate_ba from numpy's PCG64 state {state_hi, state_lo, inc_hi,
  * inc_lo, has_uint32, uinteger} (host memory).  edges_out == NULL returns E. */
@@ -417,6 +477,18 @@ int s2v_comm_allgather_slots(void *comm, void *recv, size_t bytes, size_t slot_s
                              int nslots, int rank, void *stream);
 int s2v_comm_allreduce(void *comm, void *buf, size_t count, int kind /*0 i64 1 f64 2 f32*/,
                        void *stream);
+/* Rank-ordered all-reduce (collective.py:100-117: result = rank 0's values,
+ * then += rank 1, rank 2, ... -- identical bits on every rank and equal to the
+ * reference's in-process sum): NCCL all-gather into scratch [P][count], then
+ * s2v_sum_ranks_typed.  The peer-memory transports push into every peer's
+ * scratch and call s2v_sum_ranks_typed directly. */
+int s2v_comm_allreduce_ordered(void *comm, void *buf, size_t count, int kind, void *scratch,
+                               void *stream);
+int s2v_sum_ranks_typed(int kind /*0 i64 1 f64 2 f32*/, int P, int64_t n, const void *gathered,
+                        void *out, void *stream);
+/* cudaDeviceEnablePeerAccess from the current device (thread-ranks of one
+ * process on different GPUs: NVLink P2P loads/stores of peer buffers). */
+int s2v_enable_peer_access(int peer_device);
 /* cudaMemcpyAsync(..., cudaMemcpyDefault): the in-process thread-group
  * transport (ranks as threads, possibly sharing one device) moves halo chunks
  * with peer copies instead of NCCL. */

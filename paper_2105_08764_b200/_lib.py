@@ -125,6 +125,9 @@ _SIGNATURES = {
     "s2v_comm_allgather": ([_P, _P, _P, _SZ, _P], _I),
     "s2v_comm_allgather_slots": ([_P, _P, _SZ, _SZ, _I, _I, _P], _I),
     "s2v_comm_allreduce": ([_P, _P, _SZ, _I, _P], _I),
+    "s2v_comm_allreduce_ordered": ([_P, _P, _SZ, _I, _P, _P], _I),
+    "s2v_sum_ranks_typed": ([_I, _I, _I64, _P, _P, _P], _I),
+    "s2v_enable_peer_access": ([_I], _I),
     "s2v_memcpy_async": ([_P, _P, _SZ, _P], _I),
     "s2v_ipc_export": ([_P, _P, ctypes.POINTER(ctypes.c_uint64)], _I),
     "s2v_ipc_import": ([_P, ctypes.POINTER(ctypes.c_void_p)], _I),
@@ -134,6 +137,9 @@ _SIGNATURES = {
     "s2v_generate_ba": ([_I64, _I64, _P, _P], _I64),
     "s2v_generate_rmat": ([_I, _I64, _P, _D, _D, _D, _I64, _P], _I64),
     "s2v_build_csr": ([_I64, _P, _I64, _P, _P], _I),
+    "s2v_shard_structure": ([_I64, _I, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P,
+                             ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32), _P],
+                            _I),
 }
 
 _lib = None
@@ -191,7 +197,8 @@ KERNELS_PER_CALL = {
     "s2v_h1_table": 1, "s2v_embed_round2_table": 1, "s2v_trow": 1, "s2v_colsum_residual": 3,
     "s2v_active_compact": 3, "s2v_score_cached": 2, "s2v_frontier_seed": 3,
     "s2v_frontier_expand": 9, "s2v_adam_pack": 2, "s2v_segment_copy": 1,
-    "s2v_merge_rank_keys": 1, "s2v_sum_ranks": 1, "s2v_sub_i64": 1,
+    "s2v_merge_rank_keys": 1, "s2v_sum_ranks": 1, "s2v_sub_i64": 1, "s2v_sum_ranks_typed": 1,
+    "s2v_comm_allreduce_ordered": 1,
     "s2v_eval_chain": 14,  # L = 5: 4 rounds, colsum 2, u1, score, merge, select, apply 3, trace
 }
 launch_count = 0

@@ -118,7 +118,20 @@ class _DeviceComm:
                        slot_stride, nslots, self.rank, stream)
 
     def allreduce(self, buf_ptr: int, count: int, kind: int, stream: int) -> None:
-        self._lib.call("s2v_comm_allreduce", self.handle, buf_ptr, count, kind, stream)
+        """Rank-ordered sum (all-gather + s2v_sum_ranks_typed), not
+        ncclAllReduce: the reference adds rank 0, 1, ... in order
+        (collective.py:114-116) and NCCL's ring order is not that."""
+        import torch
+        if count == 0:
+            return
+        nbytes = count * (4 if kind == 2 else 8)
+        buf = self._scratch.get(nbytes) if hasattr(self, "_scratch") else None
+        if buf is None:
+            self._scratch = getattr(self, "_scratch", {})
+            buf = self._scratch[nbytes] = torch.empty(self.world * nbytes, dtype=torch.uint8,
+                                                      device="cuda")
+        self._lib.call("s2v_comm_allreduce_ordered", self.handle, buf_ptr, count, kind,
+                       buf.data_ptr(), stream)
 
     def close(self) -> None:
         if self.handle:
@@ -126,82 +139,152 @@ class _DeviceComm:
             self.handle = None
 
 
-class _LocalDeviceComm:
-    """Device transport for thread-ranks of one process (run_workers).
+class _PeerTransport:
+    """Peer-memory device transport (NVLink P2P loads/stores between ranks).
 
-    Ranks may share one GPU (tests on a single B200) or own one each.  The
-    in-place halo all-gather is done with peer copies ordered by CUDA events
-    exchanged through the host rendezvous; all-reduces of the small integer /
-    fp64 packs go through the host in ascending rank order (the reference's
-    own reduction order, collective.py:114-116).
+    Every rank maps its peers' same-role buffers (peers_of: a collective
+    registration, cached per workspace by the callers); the forward round
+    kernel pushes each output row into every peer's halo buffer itself
+    (s2v_embed_round_peers -- the exchange is fused into the compute), and
+    ranks order producer/consumer with per-peer flags written and waited on
+    by the CUDA streams (no host barrier, no host synchronisation, no SM
+    spinning).  All-reduces push each rank's vector into every peer's
+    scratch row [rank] and sum the P rows in ascending rank order on the
+    device (s2v_sum_ranks_typed): the reference's order
+    (collective.py:100-117), identical bits on every rank.
+    Subclasses supply peers_of (thread-ranks: plain addresses exchanged
+    through the host rendezvous; process ranks: CUDA IPC handles).
     """
 
+    supports_push = True
+
+    def _init_flags(self):
+        import torch
+        self.epoch = 0
+        self.flags = torch.zeros(max(self.world, 1) * 8, dtype=torch.int32, device="cuda")
+        self.peer_flags = self.peers_of(self.flags)
+        self._scratch: dict = {}
+
+    def peers_of(self, tensor) -> list[int]:  # pragma: no cover - abstract
+        raise NotImplementedError
+
+    def peer_array(self, tensor):
+        """peers_of as a device array of pointers (kernel argument)."""
+        import torch
+        return torch.tensor(self.peers_of(tensor), dtype=torch.int64, device=tensor.device)
+
+    def signal_and_wait(self, stream: int) -> None:
+        """Stream-ordered all-rank barrier: after this rank's prior work, raise
+        its flag in every peer; before later work, wait for every peer's."""
+        self.epoch += 1
+        for q in range(self.world):
+            self._lib.call("s2v_stream_write_u32", self.peer_flags[q] + 4 * self.rank,
+                           self.epoch, stream)
+        own = self.flags.data_ptr()
+        for q in range(self.world):
+            self._lib.call("s2v_stream_wait_u32", own + 4 * q, self.epoch, stream)
+
+    def allgather_rows(self, tensor, chunk_bytes: int, slot_stride: int, nslots: int,
+                       stream: int, peers=None) -> None:
+        """Pull every peer's chunk of each slot (generic layouts; the K = 64
+        rounds push instead)."""
+        if peers is None:
+            peers = self.peers_of(tensor)
+        self.signal_and_wait(stream)  # every producer is done
+        own = tensor.data_ptr()
+        for q in range(self.world):
+            if q == self.rank:
+                continue
+            for b in range(nslots):
+                off = b * slot_stride + q * chunk_bytes
+                self._lib.call("s2v_memcpy_async", own + off, peers[q] + off, chunk_bytes, stream)
+        self.signal_and_wait(stream)  # every reader is done before buffers are reused
+
+    def allreduce(self, buf_ptr: int, count: int, kind: int, stream: int) -> None:
+        """In-place ascending-rank sum of count elements (kind 0 int64,
+        1 fp64, 2 fp32) across the ranks, entirely on the device.  Two scratch
+        buffers per (count, kind) alternate: the signal of the next
+        all-reduce separates a reuse from every peer's read of it."""
+        import torch
+        if count == 0:
+            return
+        item = 4 if kind == 2 else 8
+        nbytes = count * item
+        ent = self._scratch.get((count, kind))
+        if ent is None:
+            bufs = [torch.empty(self.world * nbytes, dtype=torch.uint8, device="cuda")
+                    for _ in range(2)]
+            ent = self._scratch[(count, kind)] = [bufs, [self.peers_of(b) for b in bufs], 0]
+        bufs, peers, par = ent
+        ent[2] ^= 1
+        for q in range(self.world):
+            self._lib.call("s2v_memcpy_async", peers[par][q] + self.rank * nbytes, buf_ptr,
+                           nbytes, stream)
+        self.signal_and_wait(stream)  # every rank's row has landed
+        self._lib.call("s2v_sum_ranks_typed", kind, self.world, count, bufs[par].data_ptr(),
+                       buf_ptr, stream)
+
+
+class _LocalDeviceComm(_PeerTransport):
+    """Peer-memory transport for thread-ranks of one process (run_workers).
+
+    Ranks may share one GPU (tests on a single B200) or own one each (peer
+    access enabled between every pair of the group's devices).  Every rank
+    runs on its own CUDA stream (run_workers), so one rank's stream waiting
+    on a flag never blocks a peer sharing the device."""
+
     def __init__(self, comm: "Comm"):
+        import torch
         from . import _lib
         self._lib = _lib
         self.comm = comm
         self.world, self.rank = comm.size, comm.rank
+        dev = torch.cuda.current_device()
+        for other in self._publish(dev):
+            _lib.call("s2v_enable_peer_access", int(other))
+        self._init_flags()
 
     def _publish(self, value):
         return self.comm.group._exchange_objects(self.rank, value)
 
-    supports_push = False
+    def _init_flags(self):
+        self.epoch = 0
+        self._scratch: dict = {}
 
-    def allgather_rows(self, tensor, chunk_bytes: int, slot_stride: int, nslots: int,
-                       stream: int, peers=None) -> None:
-        self.allgather_slots(tensor.data_ptr(), chunk_bytes, slot_stride, nslots, stream)
-
-    def allgather_slots(self, buf_ptr: int, chunk_bytes: int, slot_stride: int, nslots: int,
-                        stream: int) -> None:
+    def signal_and_wait(self, stream: int) -> None:
+        """Stream-ordered all-rank barrier with CUDA events: each rank records
+        an event after its prior work and its stream waits on every peer's.
+        (Stream waits on peer-written flags can deadlock when thread-ranks
+        share a device: their streams may share a hardware queue.)  The host
+        threads only exchange the event handles; no GPU work is waited on."""
         import torch
-        ready = torch.cuda.Event()
-        ready.record()
-        peers = self._publish((buf_ptr, ready))
-        for q, (peer_ptr, peer_ready) in enumerate(peers):
-            if q == self.rank:
-                continue
-            torch.cuda.current_stream().wait_event(peer_ready)
-            for b in range(nslots):
-                off = b * slot_stride + q * chunk_bytes
-                self._lib.call("s2v_memcpy_async", buf_ptr + off, peer_ptr + off, chunk_bytes,
-                               stream)
-        done = torch.cuda.Event()
-        done.record()
-        for q, ev in enumerate(self._publish(done)):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.ExternalStream(stream))
+        for q, peer_ev in enumerate(self._publish(ev)):
             if q != self.rank:
-                torch.cuda.current_stream().wait_event(ev)
+                torch.cuda.ExternalStream(stream).wait_event(peer_ev)
 
-    def allreduce(self, buf_ptr: int, count: int, kind: int, stream: int) -> None:
-        _host_allreduce(self._lib, self.comm, buf_ptr, count, kind, stream)
+    def peers_of(self, tensor) -> list[int]:
+        """Every rank's address of the same-role buffer (own included);
+        collective, same contract as the IPC transport's."""
+        return [int(p) for p in self._publish(tensor.data_ptr())]
 
     def close(self) -> None:
         pass
 
 
-class _IpcDeviceComm:
-    """Peer-memory transport for process ranks (torchrun / DistComm).
-
-    Halo buffers are mapped into every peer with CUDA IPC; the forward round
-    kernel pushes each output row into all peers' buffers itself
-    (s2v_embed_round_peers -- the exchange is fused into the compute), and
-    ranks order producer/consumer through per-peer flags written and waited
-    on by the CUDA streams (no host barrier, no SM spinning).  Ranks may
-    share a GPU (tests) or own one each (NVLink P2P).  Generic layouts fall
-    back to pulling peers' chunks with copies between two flag epochs.
-    """
-
-    supports_push = True
+class _IpcDeviceComm(_PeerTransport):
+    """Peer-memory transport for process ranks (torchrun / DistComm): peer
+    buffers mapped with CUDA IPC.  Ranks may share a GPU (tests) or own one
+    each (NVLink P2P)."""
 
     def __init__(self, comm: "DistComm"):
-        import torch
         from . import _lib
         self._lib = _lib
         self.comm = comm
         self.world, self.rank = comm.size, comm.rank
         self._imports: dict[bytes, int] = {}
-        self.epoch = 0
-        self.flags = torch.zeros(max(self.world, 1) * 8, dtype=torch.int32, device="cuda")
-        self.peer_flags = self.peers_of(self.flags)
+        self._init_flags()
 
     def _export(self, ptr: int):
         handle = ctypes.create_string_buffer(64)
@@ -230,55 +313,10 @@ class _IpcDeviceComm:
         return [tensor.data_ptr() if q == self.rank else self._import(h) + o
                 for q, (h, o) in enumerate(allh)]
 
-    def peer_array(self, tensor):
-        """peers_of as a device array of pointers (kernel argument)."""
-        import torch
-        return torch.tensor(self.peers_of(tensor), dtype=torch.int64, device=tensor.device)
-
-    def signal_and_wait(self, stream: int) -> None:
-        """Stream-ordered all-rank barrier: after this rank's prior work, raise
-        its flag in every peer; before later work, wait for every peer's."""
-        self.epoch += 1
-        for q in range(self.world):
-            self._lib.call("s2v_stream_write_u32", self.peer_flags[q] + 4 * self.rank,
-                           self.epoch, stream)
-        own = self.flags.data_ptr()
-        for q in range(self.world):
-            self._lib.call("s2v_stream_wait_u32", own + 4 * q, self.epoch, stream)
-
-    def allgather_rows(self, tensor, chunk_bytes: int, slot_stride: int, nslots: int,
-                       stream: int, peers=None) -> None:
-        if peers is None:
-            raise ValueError("IPC all-gather needs the buffer's registered peer list")
-        self.signal_and_wait(stream)  # every producer is done
-        own = tensor.data_ptr()
-        for q in range(self.world):
-            if q == self.rank:
-                continue
-            for b in range(nslots):
-                off = b * slot_stride + q * chunk_bytes
-                self._lib.call("s2v_memcpy_async", own + off, peers[q] + off, chunk_bytes, stream)
-        self.signal_and_wait(stream)  # every reader is done before buffers are reused
-
-    def allreduce(self, buf_ptr: int, count: int, kind: int, stream: int) -> None:
-        _host_allreduce(self._lib, self.comm, buf_ptr, count, kind, stream)
-
     def close(self) -> None:
         for base in self._imports.values():
             self._lib.load().s2v_ipc_close(base)
         self._imports.clear()
-
-
-def _host_allreduce(lib, comm, buf_ptr: int, count: int, kind: int, stream: int) -> None:
-    import torch
-    dt = {0: torch.int64, 1: torch.float64, 2: torch.float32}[kind]
-    host = torch.empty(count, dtype=dt)
-    lib.call("s2v_memcpy_async", host.data_ptr(), buf_ptr, count * host.element_size(), stream)
-    torch.cuda.current_stream().synchronize()
-    total = comm.all_reduce_sum(host.numpy().copy(), tag="device")
-    host.copy_(torch.from_numpy(np.ascontiguousarray(total, dtype=host.numpy().dtype)))
-    lib.call("s2v_memcpy_async", buf_ptr, host.data_ptr(), count * host.element_size(), stream)
-    torch.cuda.current_stream().synchronize()
 
 
 def _new_unique_id() -> bytes:
@@ -451,7 +489,21 @@ def run_workers(num_workers: int, fn, *args, timeout: float = DEFAULT_TIMEOUT,
     def runner(rank: int) -> None:
         try:
             bind(rank)
-            results[rank] = fn(group.comm(rank), *args)
+            stream = None
+            if bind_devices:
+                import torch
+                if torch.cuda.is_available():
+                    # one stream per rank: the device transports order ranks
+                    # with stream waits on flags, which must never block a
+                    # peer rank sharing the device
+                    stream = torch.cuda.Stream()
+            if stream is None:
+                results[rank] = fn(group.comm(rank), *args)
+            else:
+                import torch
+                with torch.cuda.stream(stream):
+                    results[rank] = fn(group.comm(rank), *args)
+                stream.synchronize()
         except BaseException as exc:  # noqa: BLE001 -- re-raised below
             with lock:
                 failures.append((rank, exc))

@@ -613,32 +613,73 @@ __global__ void __launch_bounds__(256, 2) layer_backward64_kernel(
       partial[(int64_t)blockIdx.x * 4096 + (4 * lo + a) * 64 + 4 * hi + c] = p4[a][c];
 }
 
-// ---------------------------------------------------------------------------
-// Layer backward with dm = dz theta4 on the 5th-generation tensor cores.
+// Layer backward on the 5th-generation tensor cores (default K = 64 fp32
+// path; S2V_BWD_TC=0 selects the FFMA kernel above).
 //
-// dm is GEMM-shaped (M = 128 rows, N = 64, K = 64) and its parity bar is
-// 1e-4, not bitwise, so it runs as tcgen05.mma kind::tf32 with 3xTF32 error
-// compensation (dz = hi + lo, theta4 = hi + lo; hi*hi + hi*lo + lo*hi,
-// fp32 accumulation in TMEM): ~2^-21 relative per product, fp32-class.
-// Operands are staged K-major in shared memory in the canonical
-// SWIZZLE_NONE core-matrix layout [k/4][row/8][8][4]; one thread issues the
-// 24 MMAs of a tile, tcgen05.commit signals an mbarrier, and warps 0-3 read
-// the 128 x 64 fp32 accumulator back with tcgen05.ld (one row per thread).
-// The dtheta4 reduction (64 x 64 over the tile rows) runs on the FFMA pipes
-// meanwhile.
+// Both contractions of a tile are GEMM-shaped and carry the 1e-4 gradient
+// bar, not bitwise, so they run as tcgen05.mma kind::tf32
+// on split operands: x = hi + lo with hi = x with the low 13 mantissa bits
+// cleared and lo = x - hi (exact), every hi/lo cross term formed -- fp32-
+// class products.  The splits are stacked along M and N so every MMA is
+// M = 128:
+//   dm^T [j'][row'] = sum_k thT [j'][k] dzS [row'][k]       (policy.py:300-303)
+//       A = thT: theta4^T hi (j' < 64) | lo (j' >= 64)        M = 128, K = 64
+//       B = dzS: dz hi (row' < 32) | lo (row' >= 32)          N = 64
+//       dm[row][j] = sum of the 4 quadrants (j | j+64) x (row | row+32)
+//   dtheta4 [k'][j'] += sum_row dzT [k'][row] mT [j'][row]  (policy.py:296-297)
+//       A = dz^T hi | lo (M = 128), B = m^T hi | lo (N = 128), K = rows
+// The tensor cores' fp32 accumulation truncates when the accumulator
+// dwarfs the products, so dtheta4 is accumulated in TMEM for kDrain tiles
+// only and then drained into an IEEE fp32 accumulator in shared memory
+// (double-buffered TMEM: the MMAs of the next group run meanwhile); over a
+// whole CTA (13.5K rows at BA(2M,16)) TMEM-only accumulation measured
+// 1.7e-4 off the reference's dtheta4, the drained one matches the FFMA path.
+// tcgen05 tf32 operands must be K-major (the MN-major encodings read back
+// zeros on B200, probed), so the staging warps write dz twice (rows x k and
+// k x rows core matrices).  Core matrix = 8 M/N-rows x 16 bytes of K; the
+// strides between core matrices are padded (dzS: K-chunk 65 x 16 B; dzT /
+// mT: 8-row group 9 x 16 B) so a warp's staging stores hit 32 distinct banks.
+//
+// Warp roles (640 threads = 5 warps per SM sub-partition at 96 registers,
+// 1 CTA per SM, 32-row tiles, tile = blockIdx.x + i * gridDim.x):
+//   warps 4-19 (staging): global loads of grad_h / h_l / dzsum / m_l three
+//     tiles ahead in registers (warp = 4 rows x 128 contiguous bytes);
+//     dz = grad_h * (h_l > 0); dzsum += dz to HBM; dzS / dzT / mT hi|lo into
+//     operand stage i % 2; arrive opfull[s]
+//   warp 0, lane 0 (MMA issue, interleaved with its epilogue one tile
+//     behind): 8 + 4 MMAs per tile; commits opfree[s] (stage reusable),
+//     d1full[b] (dm accumulator complete) and, every kDrain tiles, d2full[g]
+//     (dtheta4 group accumulator complete)
+//   warps 0-3 (epilogue, TMEM lanes 32 w + [0, 32)): dm^T via tcgen05.ld,
+//     quadrant sums through shared memory, coalesced dm stores; dtheta4
+//     group drains; finally the dtheta4 partial of the CTA.
 // ---------------------------------------------------------------------------
-constexpr int kTC = 128;  // rows per tile = MMA M
+constexpr int kTR = 32;                       // rows per tile
+constexpr int kTcThreads = 640;               // 20 warps: 5 per SM sub-partition
+constexpr int kDrain = 8;                     // tiles per TMEM dtheta4 group
+constexpr uint32_t kLboS = 65 * 16;           // dzS K-chunk stride
+constexpr uint32_t kSboT = 9 * 16;            // dzT / mT 8-row (M/N) group stride
+constexpr uint32_t kLboT = 16 * kSboT;        // dzT / mT K-chunk (4 rows) stride
+constexpr uint32_t kZsBytes = 16640;          // 15 kLboS + 8 x 128, rounded to 128
+constexpr uint32_t kZtBytes = 8 * kLboT;      // 18432
+constexpr uint32_t kThBytes = 32768;          // thT: [k/4][j'/8][8][4]
+constexpr uint32_t kStageBytes = kZsBytes + 2 * kZtBytes;
+constexpr uint32_t kEpiBytes = 32 * 132 * 4;  // dm^T row sums [32 rows][132]
+constexpr uint32_t kAccBytes = 128 * 65 * 4;  // dtheta4 fp32 accumulator [128 k'][65]
+constexpr size_t kTcSmem = 128 + kThBytes + 2 * kStageBytes + kEpiBytes + kAccBytes;
 
 __device__ __forceinline__ float tf32_hi(float v) {
   return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
 }
 
-__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// SWIZZLE_NONE K-major shared-memory matrix descriptor (sm_100 version 1):
+// start, leading (K-chunk) and stride (8-row group) byte offsets
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); layout SWIZZLE_NONE
+  d |= (uint64_t)1 << 46;
   return d;
 }
 
@@ -648,6 +689,20 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
@@ -663,163 +718,249 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
   }
 }
 
-__global__ void __launch_bounds__(256, 1) layer_backward64_tc_kernel(
+// 32 consecutive fp32 TMEM columns of this warp's 32 lanes
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) layer_backward64_tc_kernel(
     s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ grad_h,
     const float *__restrict__ h_l, const float *__restrict__ m_l, float *__restrict__ dzsum,
     float *__restrict__ partial, int first, float *__restrict__ dm_out) {
-  extern __shared__ __align__(1024) float tc_smem[];
-  float *a_hi = tc_smem;               // [16][16][8][4]
-  float *a_lo = a_hi + kTC * 64;
-  float *b_hi = a_lo + kTC * 64;       // [16][8][8][4]
-  float *b_lo = b_hi + 64 * 64;
-  float(*dzs)[68] = reinterpret_cast<float(*)[68]>(b_lo + 64 * 64);
-  float(*ms)[68] = reinterpret_cast<float(*)[68]>(b_lo + 64 * 64 + kTC * 68);
-  __shared__ __align__(8) uint64_t mbar;
+  extern __shared__ uint8_t tc_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>(((uintptr_t)tc_raw + 127) & ~(uintptr_t)127);
+  float *th = reinterpret_cast<float *>(base);
+  auto stage_ptr = [&](int s) { return base + kThBytes + (uint32_t)s * kStageBytes; };
+  float *epi = reinterpret_cast<float *>(base + kThBytes + 2 * kStageBytes);  // [32][132]
+  float *acc = epi + kEpiBytes / 4;                                           // [128][65]
+  __shared__ __align__(8) uint64_t bars[12];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // B = theta4^T (n = j, k), K-major, split hi / lo
-  for (int idx = tid; idx < 64 * 64; idx += 256) {
-    const int j = idx >> 6, k = idx & 63;
-    const float v = theta4[k * 64 + j];
-    const float hi = tf32_hi(v);
-    const int off = (((k >> 2) * 8 + (j >> 3)) * 8 + (j & 7)) * 4 + (k & 3);
-    b_hi[off] = hi;
-    b_lo[off] = v - hi;
+  const bool want_dm = dm_out != nullptr, want_p4 = m_l != nullptr;
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
+  auto opfull = [&](int s) { return bar0 + 8 * s; };
+  auto opfree = [&](int s) { return bar0 + 16 + 8 * s; };
+  auto d1full = [&](int b) { return bar0 + 32 + 8 * b; };
+  auto d1free = [&](int b) { return bar0 + 48 + 8 * b; };
+  auto d2full = [&](int b) { return bar0 + 64 + 8 * b; };
+  auto d2free = [&](int b) { return bar0 + 80 + 8 * b; };
+  // thT[j'][k]: theta4[k][j' mod 64], hi for j' < 64, lo for j' >= 64
+  for (int idx = tid; idx < 128 * 64; idx += kTcThreads) {
+    const int jp = idx >> 6, k = idx & 63;
+    const float v = theta4[k * 64 + (jp & 63)], h = tf32_hi(v);
+    th[((k >> 2) * 16 + (jp >> 3)) * 32 + (jp & 7) * 4 + (k & 3)] = jp < 64 ? h : v - h;
   }
-  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&mbar);
+  for (int idx = tid; idx < 128 * 65; idx += kTcThreads) acc[idx] = 0.f;
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    for (int s = 0; s < 2; s++) {
+      mbar_init(opfull(s), 512);
+      mbar_init(opfree(s), 1);
+      mbar_init(d1full(s), 1);
+      mbar_init(d1free(s), 128);
+      mbar_init(d2full(s), 1);
+      mbar_init(d2free(s), 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_slot;
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (8u << 17) | (8u << 24);
-  const uint32_t sa_hi = (uint32_t)__cvta_generic_to_shared(a_hi);
-  const uint32_t sa_lo = (uint32_t)__cvta_generic_to_shared(a_lo);
-  const uint32_t sb_hi = (uint32_t)__cvta_generic_to_shared(b_hi);
-  const uint32_t sb_lo = (uint32_t)__cvta_generic_to_shared(b_lo);
-  const int lo = tid & 15, hi = tid >> 4;
-  float p4[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; a++)
-#pragma unroll
-    for (int c = 0; c < 4; c++)
-      p4[a][c] = first ? 0.f : partial[(int64_t)blockIdx.x * 4096 + (4 * lo + a) * 64 + 4 * hi + c];
-  uint32_t phase = 0;
+  const uint32_t tmem = tmem_slot;  // D1: cols [64 b, +64); D2: cols 128 + [128 g, +128)
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
-  const int64_t ntiles = (nrows + kTC - 1) / kTC;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * kTC;
-    __syncthreads();
-    // all of this thread's loads first (8 x 4 float4 in flight), then compute
-    float4 G[kTC / 16], H[kTC / 16], O[kTC / 16], M[kTC / 16];
+  const int64_t ntiles = (nrows + kTR - 1) / kTR;
+  const int n_my = blockIdx.x < ntiles ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  auto tile_row0 = [&](int i) { return (blockIdx.x + (int64_t)i * gridDim.x) * kTR; };
+
+  if (warp >= 4) {
+    // ---------------- staging: warp -> rows 4 (w / 2) + [0, 4), float4 columns
+    // 8 (w % 2) + [0, 8); lane -> row + (lane / 8), float4 c4 = ... + lane % 8
+    const int w = warp - 4;
+    const int row = 4 * (w >> 1) + (lane >> 3), c4 = 8 * (w & 1) + (lane & 7);
+    const int kc = 4 * c4;  // first k (or j) of the float4
+    float4 G[3], H[3], O[3], M[3];
+    auto load = [&](int i, float4 &g, float4 &hv, float4 &o, float4 &mv) {
+      const int64_t r = tile_row0(i) + row;
+      g = hv = o = mv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < n_my && r < nrows) {
+        g = f4(grad_h + r * 64 + kc);
+        hv = f4(h_l + phys_of_row(sh, r) * 64 + kc);
+        if (!first) o = f4(dzsum + r * 64 + kc);
+        if (want_p4) mv = f4(m_l + r * 64 + kc);
+      }
+    };
 #pragma unroll
-    for (int q = 0; q < kTC / 16; q++) {
-      const int e = tid + q * 256, row = e >> 4, c4 = e & 15;
-      const int64_t r = r0 + row;
-      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      G[q] = H[q] = O[q] = M[q] = z4;
-      if (r < nrows) {
-        G[q] = f4(grad_h + r * 64 + 4 * c4);
-        H[q] = f4(h_l + phys_of_row(sh, r) * 64 + 4 * c4);
-        if (!first) O[q] = f4(dzsum + r * 64 + 4 * c4);
-        if (m_l) M[q] = f4(m_l + r * 64 + 4 * c4);
+    for (int u = 0; u < 3; u++) load(u, G[u], H[u], O[u], M[u]);
+    // core-matrix offsets (floats) of this thread's elements
+    const uint32_t o_zs = (uint32_t)c4 * (kLboS / 4) + (row >> 3) * 32 + (row & 7) * 4;
+    const uint32_t o_zt = (row >> 2) * (kLboT / 4) + (row & 3);
+#pragma unroll 1
+    for (int i0 = 0; i0 < n_my; i0 += 3) {
+#pragma unroll
+      for (int u = 0; u < 3; u++) {
+        const int i = i0 + u;
+        if (i >= n_my) break;
+        const int s = i & 1;
+        const int64_t r = tile_row0(i) + row;
+        const float4 g = G[u], hv = H[u], o = O[u], mv = M[u];
+        float dz[4] = {hv.x > 0.f ? g.x : 0.f, hv.y > 0.f ? g.y : 0.f, hv.z > 0.f ? g.z : 0.f,
+                       hv.w > 0.f ? g.w : 0.f};
+        if (r < nrows)
+          st4(dzsum + r * 64 + kc,
+              make_float4(o.x + dz[0], o.y + dz[1], o.z + dz[2], o.w + dz[3]));
+        float dh[4], dl[4], mh[4], ml[4];
+        const float m4[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          dh[q] = tf32_hi(dz[q]);
+          dl[q] = dz[q] - dh[q];
+          mh[q] = tf32_hi(m4[q]);
+          ml[q] = m4[q] - mh[q];
+        }
+        load(i + 3, G[u], H[u], O[u], M[u]);  // this set is consumed: refill
+        if (i >= 2) mbar_wait(opfree(s), ((i >> 1) - 1) & 1);
+        uint8_t *sp = stage_ptr(s);
+        float *zs = reinterpret_cast<float *>(sp);
+        float *zt = reinterpret_cast<float *>(sp + kZsBytes);
+        float *mt = reinterpret_cast<float *>(sp + kZsBytes + kZtBytes);
+        // dzS [row'][k]: hi at row' = row, lo at row' = row + 32 (4 groups of 8 on)
+        st4(zs + o_zs, make_float4(dh[0], dh[1], dh[2], dh[3]));
+        st4(zs + o_zs + 4 * 32, make_float4(dl[0], dl[1], dl[2], dl[3]));
+        // dzT [k'][row] / mT [j'][row]: lo at k' + 64 (8 groups of 8 on)
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int kk = kc + q;
+          const uint32_t off = o_zt + (kk >> 3) * (kSboT / 4) + (kk & 7) * 4;
+          zt[off] = dh[q];
+          zt[off + 8 * (kSboT / 4)] = dl[q];
+          if (want_p4) {
+            mt[off] = mh[q];
+            mt[off + 8 * (kSboT / 4)] = ml[q];
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(opfull(s));
       }
     }
+  } else {
+    // ---------------- epilogue (warps 0-3: TMEM lanes 32 w + [0, 32)); warp 0
+    // lane 0 also issues the MMAs of tile i before the epilogue of tile i - 1
+    const int jp = 32 * warp + lane;  // j' of dm^T, k' of dtheta4
+    const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
+    const uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | (8u << 17) | (8u << 24);
+    const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | (16u << 17) | (8u << 24);
+    const uint32_t s_th = (uint32_t)__cvta_generic_to_shared(th);
+#pragma unroll 1
+    for (int it = 0; it <= n_my; it++) {
+      if (warp == 0 && lane == 0 && it < n_my) {
+        const int i = it;
+        const int s = i & 1, b = i & 1, grp = i / kDrain, gb = grp & 1;
+        const bool g_first = i % kDrain == 0, g_last = i % kDrain == kDrain - 1 || i == n_my - 1;
+        mbar_wait(opfull(s), (i >> 1) & 1);
+        if (i >= 2 && want_dm) mbar_wait(d1free(b), ((i >> 1) - 1) & 1);
+        if (want_p4 && g_first && grp >= 2) mbar_wait(d2free(gb), ((grp >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t sp = (uint32_t)__cvta_generic_to_shared(stage_ptr(s));
+        const uint32_t s_zs = sp, s_zt = sp + kZsBytes, s_mt = sp + kZsBytes + kZtBytes;
+        if (want_dm) {
 #pragma unroll
-    for (int q = 0; q < kTC / 16; q++) {
-      const int e = tid + q * 256, row = e >> 4, c4 = e & 15;
-      const int64_t r = r0 + row;
-      float4 dz;
-      dz.x = H[q].x > 0.f ? G[q].x : 0.f;
-      dz.y = H[q].y > 0.f ? G[q].y : 0.f;
-      dz.z = H[q].z > 0.f ? G[q].z : 0.f;
-      dz.w = H[q].w > 0.f ? G[q].w : 0.f;
-      if (r < nrows)
-        st4(dzsum + r * 64 + 4 * c4, make_float4(O[q].x + dz.x, O[q].y + dz.y, O[q].z + dz.z,
-                                                 O[q].w + dz.w));
-      st4(&dzs[row][4 * c4], dz);
-      st4(&ms[row][4 * c4], M[q]);
-      const int aoff = ((c4 * 16 + (row >> 3)) * 8 + (row & 7)) * 4;
-      const float4 h4 = make_float4(tf32_hi(dz.x), tf32_hi(dz.y), tf32_hi(dz.z), tf32_hi(dz.w));
-      st4(a_hi + aoff, h4);
-      st4(a_lo + aoff, make_float4(dz.x - h4.x, dz.y - h4.y, dz.z - h4.z, dz.w - h4.w));
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (dm_out && tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t as[3] = {sa_hi, sa_hi, sa_lo};
-      const uint32_t bs[3] = {sb_hi, sb_lo, sb_hi};
+          for (int ks = 0; ks < 8; ks++)  // K = 8 of k per MMA
+            mma_tf32(tmem + 64 * b, umma_desc(s_th + ks * 2 * 2048, 2048, 128),
+                     umma_desc(s_zs + ks * 2 * kLboS, kLboS, 128), idesc1, ks ? 1u : 0u);
+        }
+        if (want_p4) {
 #pragma unroll
-      for (int sk = 0; sk < 8; sk++)
-#pragma unroll
-        for (int q = 0; q < 3; q++)
-          mma_tf32(tmem, umma_desc_kmajor(as[q] + sk * 2 * 2048, 2048, 128),
-                   umma_desc_kmajor(bs[q] + sk * 2 * 1024, 1024, 128), idesc,
-                   (sk | q) ? 1u : 0u);
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
-                       "r"(bar)
-                   : "memory");
-    }
-    if (m_l) {
-#pragma unroll 4
-      for (int row = 0; row < kTC; row++) {
-        const float4 d = f4(&dzs[row][4 * lo]);
-        const float4 m = f4(&ms[row][4 * hi]);
-        const float dv[4] = {d.x, d.y, d.z, d.w}, mvv[4] = {m.x, m.y, m.z, m.w};
-#pragma unroll
-        for (int a = 0; a < 4; a++)
-#pragma unroll
-          for (int c = 0; c < 4; c++) p4[a][c] = __fmaf_rn(dv[a], mvv[c], p4[a][c]);
+          for (int ks = 0; ks < 4; ks++)  // K = 8 rows per MMA
+            mma_tf32(tmem + 128 + 128 * gb, umma_desc(s_zt + ks * 2 * kLboT, kLboT, kSboT),
+                     umma_desc(s_mt + ks * 2 * kLboT, kLboT, kSboT), idesc2,
+                     (!g_first || ks) ? 1u : 0u);
+        }
+        mma_commit(opfree(s));
+        mma_commit(d1full(b));
+        if (want_p4 && g_last) mma_commit(d2full(gb));
       }
-    }
-    if (dm_out) {
-      mbar_wait(bar, phase);
-      phase ^= 1;
+      __syncwarp();
+      if (it == 0) continue;
+      const int i = it - 1;
+      const int b = i & 1, grp = i / kDrain, gb = grp & 1;
+      const bool g_last = i % kDrain == kDrain - 1 || i == n_my - 1;
+      mbar_wait(d1full(b), (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      if (warp < 4) {
-        const int64_t r = r0 + 32 * warp + lane;
+      if (want_dm) {
+        {
+          float hi[32], lo[32];
+          tmem_ld32(tmem + lane_base + 64 * b, hi);       // row' = row (dz hi)
+          tmem_ld32(tmem + lane_base + 64 * b + 32, lo);  // row' = row + 32 (dz lo)
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          mbar_arrive(d1free(b));
+          named_sync(1, 128);  // the previous tile's epi reads are done
 #pragma unroll
-        for (int cb = 0; cb < 4; cb++) {
-          uint32_t v[16];
-          const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + 16 * cb;
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
-              "%10, %11, %12, %13, %14, %15}, [%16];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-              : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (r < nrows) {
-            float *dst = dm_out + phys_of_row(sh, r) * 64 + 16 * cb;
+          for (int rr = 0; rr < 32; rr++) epi[rr * 132 + jp] = hi[rr] + lo[rr];
+        }
+        named_sync(1, 128);
+        // dm[row][j] = epi[row][j] + epi[row][j + 64]: thread -> row tid / 4,
+        // columns 16 (tid % 4) + [0, 16)
+        const int rr = tid >> 2, j0 = 16 * (tid & 3);
+        const int64_t r = tile_row0(i) + rr;
+        if (r < nrows) {
+          float *dst = dm_out + phys_of_row(sh, r) * 64 + j0;
+          const float *e = epi + rr * 132 + j0;
 #pragma unroll
-            for (int q = 0; q < 4; q++)
-              st4(dst + 4 * q, make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                           __uint_as_float(v[4 * q + 2]),
-                                           __uint_as_float(v[4 * q + 3])));
+          for (int q = 0; q < 4; q++) {
+            const float4 a = f4(e + 4 * q), c = f4(e + 64 + 4 * q);
+            st4(dst + 4 * q, make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w));
           }
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
+      if (want_p4 && g_last) {  // drain the group's dtheta4 into the fp32 accumulator
+        mbar_wait(d2full(gb), (grp >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+        for (int h = 0; h < 2; h++) {
+          float a[32], c[32];
+          tmem_ld32(tmem + lane_base + 128 + 128 * gb + 32 * h, a);
+          tmem_ld32(tmem + lane_base + 128 + 128 * gb + 64 + 32 * h, c);
+#pragma unroll
+          for (int q = 0; q < 32; q++) acc[jp * 65 + 32 * h + q] += a[q] + c[q];
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        mbar_arrive(d2free(gb));
+      }
     }
   }
-#pragma unroll
-  for (int a = 0; a < 4; a++)
-#pragma unroll
-    for (int c = 0; c < 4; c++)
-      partial[(int64_t)blockIdx.x * 4096 + (4 * lo + a) * 64 + 4 * hi + c] = p4[a][c];
+  // ---------------- dtheta4 partial of this CTA: acc[k][j] + acc[k + 64][j]
+  __syncthreads();
+  for (int idx = tid; idx < 4096; idx += kTcThreads) {
+    const int k = idx >> 6, j = idx & 63;
+    float *dst = partial + (int64_t)blockIdx.x * 4096 + idx;
+    *dst = (first ? 0.f : *dst) + (acc[k * 65 + j] + acc[(k + 64) * 65 + j]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // dtheta1 [64], dtheta2 [64], dtheta3 [64][64] partials from dzsum.
@@ -1135,17 +1276,17 @@ template <class T>
 static int layer_backward_t(const s2v_shard *sh, int K, const void *theta4, const void *grad_h,
                             const void *h_l, const void *m_l, void *dzsum, void *partial,
                             int first, void *dm_out, cudaStream_t st) {
-  // tcgen05 3xTF32 dm path: parity-verified, opt-in (S2V_BWD_TC=1) because
-  // at 1 CTA/SM it measures slower than the FFMA kernel
+  // tcgen05 path by default for K = 64 fp32; S2V_BWD_TC=0 selects the FFMA
+  // kernel (kept as the cross-check of the tensor-core path)
   static const bool use_tc = [] {
     const char *e = getenv("S2V_BWD_TC");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   if (sizeof(T) == 4 && K == 64 && use_tc) {
-    const size_t smem = sizeof(float) * (2 * kTC * 64 + 2 * 64 * 64 + 2 * kTC * 68);
     S2V_CUDA_CHECK(cudaFuncSetAttribute(layer_backward64_tc_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    layer_backward64_tc_kernel<<<bwd_blocks(*sh), 256, smem, st>>>(
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kTcSmem));
+    layer_backward64_tc_kernel<<<bwd_blocks(*sh), kTcThreads, kTcSmem, st>>>(
         *sh, (const float *)theta4, (const float *)grad_h, (const float *)h_l,
         (const float *)m_l, (float *)dzsum, (float *)partial, first, (float *)dm_out);
     S2V_LAUNCH_CHECK();

@@ -7,11 +7,30 @@
 #include <cuda.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "s2v_common.cuh"
 
 using namespace s2v;
+
+namespace {
+
+// out[i] = ((g[0][i] + g[1][i]) + g[2][i]) + ...: the reference's all-reduce
+// order (collective.py:114-116: out = slots[0].astype(...); out += other for
+// the later ranks), so every rank computes the same bits as the reference.
+template <class T>
+__global__ void sum_ranks_typed_kernel(int P, int64_t n, const T *__restrict__ g,
+                                       T *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    T acc = g[i];
+    for (int r = 1; r < P; r++) acc = acc + g[(int64_t)r * n + i];
+    out[i] = acc;
+  }
+}
+
+}  // namespace
 
 typedef CUresult (*PFN_addr_range)(CUdeviceptr *, size_t *, CUdeviceptr);
 typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
@@ -145,6 +164,56 @@ int s2v_stream_wait_u32(void *addr, uint32_t value, void *stream) {
 int s2v_memcpy_async(void *dst, const void *src, size_t bytes, void *stream) {
   S2V_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)));
   return S2V_OK;
+}
+
+int s2v_sum_ranks_typed(int kind, int P, int64_t n, const void *gathered, void *out,
+                        void *stream) {
+  if (n <= 0) return S2V_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 1024);
+  cudaStream_t st = as_stream(stream);
+  if (kind == 0)
+    sum_ranks_typed_kernel<int64_t><<<grid, 256, 0, st>>>(P, n, (const int64_t *)gathered,
+                                                          (int64_t *)out);
+  else if (kind == 1)
+    sum_ranks_typed_kernel<double><<<grid, 256, 0, st>>>(P, n, (const double *)gathered,
+                                                         (double *)out);
+  else if (kind == 2)
+    sum_ranks_typed_kernel<float><<<grid, 256, 0, st>>>(P, n, (const float *)gathered,
+                                                        (float *)out);
+  else
+    return fail(S2V_EINVAL, "sum_ranks: unknown kind %d", kind);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
+int s2v_enable_peer_access(int peer_device) {
+  int cur = 0;
+  S2V_CUDA_CHECK(cudaGetDevice(&cur));
+  if (peer_device == cur) return S2V_OK;
+  int can = 0;
+  S2V_CUDA_CHECK(cudaDeviceCanAccessPeer(&can, cur, peer_device));
+  if (!can) return fail(S2V_ECOMM, "device %d cannot access peer device %d", cur, peer_device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return S2V_OK;
+  }
+  S2V_CUDA_CHECK(e);
+  return S2V_OK;
+}
+
+// Rank-ordered all-reduce over NCCL: all-gather every rank's count elements
+// into scratch [P][count], then the ascending-rank sum (sum_ranks) into buf.
+int s2v_comm_allreduce_ordered(void *comm, void *buf, size_t count, int kind, void *scratch,
+                               void *stream) {
+  int P = 0, rank = 0;
+  ncclCommCount((ncclComm_t)comm, &P);
+  ncclCommUserRank((ncclComm_t)comm, &rank);
+  const size_t bytes = count * (kind == 2 ? 4 : 8);
+  ncclResult_t r = ncclAllGather(buf, scratch, bytes, ncclUint8, (ncclComm_t)comm,
+                                 as_stream(stream));
+  if (r != ncclSuccess) return fail(S2V_ECOMM, "ncclAllGather: %s", ncclGetErrorString(r));
+  return s2v_sum_ranks_typed(kind, P, (int64_t)count, scratch, buf, stream);
 }
 
 int s2v_comm_allreduce(void *comm, void *buf, size_t count, int kind, void *stream) {

@@ -260,6 +260,10 @@ def _allgather_rows(state: PartitionedState, comm, h: torch.Tensor, k: int, tag:
 # previous round from HBM appends (start, end) CUDA events recorded on the
 # launching stream around its kernel (the degree-table round 2 is not one)
 ROUND_TIMER = None
+# bench hook: when a list, loss_and_gradients appends (tag, start, end) around
+# every s2v_layer_backward (tag: ("layer_backward", first, has_m, has_dm)) and
+# s2v_gather (("gather",)) launch
+BWD_TIMER = None
 
 
 def _degree_table_round2(state: PartitionedState, k: int, dt: int, num_layers: int,
@@ -693,16 +697,30 @@ def _loss_pack(state: PartitionedState, actions: np.ndarray, targets: np.ndarray
     comm.record("q_bwd", b * k)
     _lib.call("s2v_grad_h_init", dt, state.shard_ref(), k, ptr(ws["dg"]), ptr(ws["actions"]),
               ptr(ws["dact"]), ptr(ws["grad_h"]), s)
+    timer = BWD_TIMER
+
+    def timed(tag, fn):
+        if timer is None:
+            return fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        timer.append((tag, e0, e1))
+
     for layer in range(L - 1, -1, -1):
         last = layer == 0
-        _lib.call("s2v_layer_backward", dt, state.shard_ref(), k, dparams.ptr("theta4"),
-                  ptr(ws["grad_h"]), ptr(hs[layer]), ptr(ms[layer]) if layer > 0 else None,
-                  ptr(ws["dzsum"]), ptr(ws["p4"]), 1 if layer == L - 1 else 0,
-                  None if last else ptr(ws["dm"]), s)
+        flags = (layer == L - 1, layer > 0, not last)  # first, m_l, dm_out
+        timed(("layer_backward",) + flags, lambda: _lib.call(
+            "s2v_layer_backward", dt, state.shard_ref(), k, dparams.ptr("theta4"),
+            ptr(ws["grad_h"]), ptr(hs[layer]), ptr(ms[layer]) if layer > 0 else None,
+            ptr(ws["dzsum"]), ptr(ws["p4"]), 1 if layer == L - 1 else 0,
+            None if last else ptr(ws["dm"]), s))
         if last:
             break
         _allgather_rows(state, comm, ws["dm"], k, "embed_bwd", name="dm")
-        _lib.call("s2v_gather", dt, state.shard_ref(), k, ptr(ws["dm"]), ptr(ws["grad_h"]), s)
+        timed(("gather",), lambda: _lib.call("s2v_gather", dt, state.shard_ref(), k,
+                                             ptr(ws["dm"]), ptr(ws["grad_h"]), s))
     # dtheta2's einsum terms go to a chain-layout buffer: grad_h is free by
     # now and has the size unless K is not a multiple of 32 / itemsize
     t2b = lib.s2v_theta2_terms_bytes(dt, state.shard_ref(), k)

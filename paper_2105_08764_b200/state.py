@@ -85,32 +85,32 @@ class _ShardStructure:
         n, p = graph.num_nodes, part.num_workers
         row_ptr_g, cols_g = graph.csr_arrays()
         lo, hi = int(row_ptr_g[part.row_start]), int(row_ptr_g[part.row_stop])
-        row_ptr = row_ptr_g[part.row_start:part.row_stop + 1] - lo
-        nbr = cols_g[lo:hi]
-        phys = phys_rows(n, p) if p > 1 else None
-        cols0 = (phys[nbr] if phys is not None else nbr).astype(np.int32)
         rows = part.num_rows
-        local_row = np.repeat(np.arange(rows, dtype=np.int32), np.diff(row_ptr))
-        order = np.argsort(nbr, kind="stable")  # by column, rows ascending
-        col_ptr = np.zeros(n + 1, dtype=np.int64)
-        np.cumsum(np.bincount(nbr, minlength=n), out=col_ptr[1:])
         self.nnz = hi - lo
         self.rows = rows
-        self.max_deg = int(np.diff(row_ptr).max()) if rows else 0
         # over the whole graph: e12 / h1 tables are indexed by the residual
         # degree of neighbours that other ranks own
         self.max_deg_global = int(np.diff(row_ptr_g).max()) if n else 0
-        # descending-degree processing order (load balance of the round
-        # kernel); rows above the hub degree go to the CTA-cooperative kernel
-        deg = np.diff(row_ptr)
-        by_degree = np.argsort(-deg, kind="stable").astype(np.int32)
-        self.n_hub = int(np.count_nonzero(deg > _lib.HUB_DEGREE))
-        self.order = to_device(by_degree, device)
-        self.row_ptr = to_device(row_ptr, device)
-        self.cols0 = to_device(cols0, device)
-        self.col_ptr = to_device(col_ptr, device)
-        self.col_ent = to_device(order.astype(np.int64), device)
-        self.col_row = to_device(local_row[order], device)
+        # the rest is built on the device (s2v_shard_structure): physical
+        # column ids, the column lookup (stable argsort by neighbour id) and
+        # the descending-degree processing order (rows above the hub degree
+        # go to the CTA-cooperative kernel)
+        self.row_ptr = to_device(row_ptr_g[part.row_start:part.row_stop + 1] - lo, device,
+                                 pinned=True)
+        nbr = to_device(cols_g[lo:hi], device, pinned=True) if self.nnz else \
+            torch.zeros(1, dtype=torch.int32, device=device)
+        self.cols0 = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=device)
+        self.col_ptr = torch.empty(n + 1, dtype=torch.int64, device=device)
+        self.col_ent = torch.empty(max(self.nnz, 1), dtype=torch.int64, device=device)
+        self.col_row = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=device)
+        self.order = torch.empty(max(rows, 1), dtype=torch.int32, device=device)
+        n_hub, max_deg = ctypes.c_int64(0), ctypes.c_int32(0)
+        _lib.call("s2v_shard_structure", n, p, rows_max_of(n, p), rows, ptr(self.row_ptr),
+                  ptr(nbr), self.nnz, ptr(self.cols0), ptr(self.col_ptr), ptr(self.col_ent),
+                  ptr(self.col_row), ptr(self.order), ctypes.byref(n_hub),
+                  ctypes.byref(max_deg), stream_ptr())
+        self.n_hub = int(n_hub.value)
+        self.max_deg = int(max_deg.value)
 
 
 def _structure(graph: Graph, part: Partition, device: torch.device) -> _ShardStructure:

@@ -95,3 +95,63 @@ def test_owner_side_rejection_under_p2():
         st.apply_action(1)
     with pytest.raises(P.InvalidActionError, match="already in the solution"):
         P.run_workers(2, worker)
+
+
+@pytest.mark.parametrize("kind,dtype", [(2, np.float32), (1, np.float64), (0, np.int64)])
+def test_device_allreduce_is_rank_ordered(kind, dtype):
+    """The peer transport's all-reduce sums rank 0, then += rank 1, rank 2 on
+    the device (collective.py:114-116): values chosen so that fp addition
+    order shows, and every rank holds the same bits as the host Comm's sum."""
+    import torch
+    from paper_2105_08764_b200.device import stream_ptr
+    rng = np.random.default_rng(11)
+    vals = [(rng.standard_normal(1000) * 10.0 ** rng.integers(-6, 7, 1000)).astype(dtype)
+            if kind else rng.integers(-2**40, 2**40, 1000) for _ in range(3)]
+    want = vals[0].copy()
+    for v in vals[1:]:
+        want += v
+
+    def worker(comm):
+        dc = comm.device_comm()
+        assert dc.supports_push
+        t = torch.from_numpy(vals[comm.rank].copy()).cuda()
+        for _ in range(3):  # alternating scratch buffers, repeated use
+            u = t.clone()
+            dc.allreduce(u.data_ptr(), u.numel(), kind, stream_ptr())
+        host = comm.all_reduce_sum(vals[comm.rank])
+        return u.cpu().numpy(), host
+    for dev_sum, host_sum in P.run_workers(3, worker):
+        assert np.array_equal(dev_sum, want)
+        assert np.array_equal(dev_sum, host_sum)
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_device_tau_loop_at_p_ranks(p):
+    """train_iterations (the device tau loop) at P thread-ranks: dg and the
+    gradient pack are all-reduced on the device, replicas end bit-identical
+    and equal to P = 1 within the gradient bar."""
+    rng = np.random.default_rng(5)
+    n, B, K, L, tau = 400, 2, 32, 3, 3
+    graphs = [P.generate_ba(n, 4, 90 + i) for i in range(B)]
+    sols = (rng.random((B, n)) < 0.1).astype(np.uint8)
+    ps = port.ResidualState([g.edge_array for g in graphs], n, solutions=sols)
+    actions = np.array([int(np.flatnonzero(ps.cand[b])[1]) for b in range(B)])
+    targets = rng.normal(size=B).astype(np.float32)
+
+    def worker(comm):
+        params = P.PolicyParams.initialize(K, L, seed=4)
+        adam = P.AdamState.create(params, lr=1e-3)
+        part = P.partition_rows(n, comm.size)[comm.rank]
+        st = P.PartitionedState(graphs, part, solutions=sols)
+        losses = P.policy.train_iterations(st, actions, targets, params, adam, tau, comm)
+        return losses, params
+    (l1, p1), = P.run_workers(1, worker)
+    outs = P.run_workers(p, worker)
+    for losses, params in outs:
+        assert np.allclose(losses, l1, rtol=1e-5)
+        for k in P.PARAM_NAMES:
+            assert scale_error(getattr(params, k), getattr(p1, k)).max() < 1e-4, k
+    for losses, params in outs[1:]:
+        assert losses == outs[0][0]
+        for k in P.PARAM_NAMES:
+            assert np.array_equal(getattr(params, k), getattr(outs[0][1], k))

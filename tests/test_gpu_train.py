@@ -154,14 +154,15 @@ def test_loss_and_gradients_with_hub_rows_vs_port():
         assert scale_error(grads[k], grads_o[k]).max() < 1e-4, k
 
 
-def test_tensor_core_backward_path_vs_port():
-    """The opt-in tcgen05 (3xTF32) dm kernel: same K=64 parity cases, run in a
-    child process because the path is chosen once per process (S2V_BWD_TC)."""
+def test_ffma_backward_path_vs_port():
+    """The FFMA layer-backward kernel (S2V_BWD_TC=0; the default K = 64 path
+    is the tcgen05 split-TF32 kernel): same K=64 parity cases, run in a child
+    process because the path is chosen once per process."""
     import os
     import subprocess
     import sys
     here = Path(__file__).resolve().parent
-    env = dict(os.environ, S2V_BWD_TC="1")
+    env = dict(os.environ, S2V_BWD_TC="0")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                         str(here / "test_gpu_train.py"), "-k",
                         "(vs_port and 64) or hub or ba1000", "-m", "gpu"],
