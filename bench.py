@@ -683,6 +683,22 @@ def main():
                 "peak_source": peak_src,
                 "bytes_model": "8(rows+1) row_ptr + 4 nnz cols + 256 alive gathers + 256 rows h_out"
                                " + 4 rows rdeg + rows sol"}
+    if world > 1:
+        # NVLink roofline of the fused halo exchange: every round pushes this
+        # rank's new rows into every peer, so each GPU receives the other
+        # ranks' rows, 4 K (N - N_loc) bytes per round,
+        # during the round kernel (round_ms includes the push)
+        recv = 4 * 64 * (graph.num_nodes - rows)
+        nv_peak = 770.0  # GB/s per direction, measured peer copy (B200_PROFILING.md)
+        nv = recv / (round_ms * 1e-3) / 1e9
+        roofline["nvlink"] = {
+            "bytes_received_per_round": recv, "achieved": round(nv, 1), "peak": nv_peak,
+            "unit": "GB/s", "frac": round(nv / nv_peak, 4),
+            "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+            "transport": type(comm.device_comm()).__name__,
+            "same_device": bool(args.same_device),
+            "note": ("ranks share one GPU: no NVLink traversed, the fraction is not an NVLink "
+                     "measurement") if args.same_device else "fused push over NVLink P2P"}
 
     # end to end through the public API: host solution vector -> state -> step
     e2e = None

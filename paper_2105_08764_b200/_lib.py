@@ -137,6 +137,25 @@ _SIGNATURES = {
     "s2v_generate_ba": ([_I64, _I64, _P, _P], _I64),
     "s2v_generate_rmat": ([_I, _I64, _P, _D, _D, _D, _I64, _P], _I64),
     "s2v_build_csr": ([_I64, _P, _I64, _P, _P], _I),
+    # handle-level API (library-owned memory; bound by plain-ctypes callers,
+    # tests/handle_abi_child.py -- the Python mirror uses the entry points
+    # above)
+    "s2v_ctx_create": ([_I, _I, _I, _P, ctypes.POINTER(ctypes.c_void_p)], _I),
+    "s2v_ctx_destroy": ([_P], _I),
+    "s2v_ctx_sync": ([_P], _I),
+    "s2v_graph_upload": ([_P, _I64, _P, _P, ctypes.POINTER(ctypes.c_void_p)], _I),
+    "s2v_graph_destroy": ([_P], _I),
+    "s2v_state_create": ([_P, _P, _I, _P, ctypes.POINTER(ctypes.c_void_p)], _I),
+    "s2v_state_destroy": ([_P], _I),
+    "s2v_state_shard": ([_P, _SH], _I),
+    "s2v_embed": ([_P, _P, _I, _P, _I, _I], _I),
+    "s2v_global_sum": ([_P, _P, _P], _I),
+    "s2v_score_topk": ([_P, _P, _I, _P, _P], _I),
+    "s2v_apply": ([_P, _P, _P, _I, _P, _P], _I),
+    "s2v_loss_grad": ([_P, _P, _I, _P, _I, _I, _P, _P, _P, ctypes.POINTER(ctypes.c_double)],
+                      _I),
+    "s2v_adam_update": ([_P, _I, _P, _P, _P, _P, _I64, _I, _D, _D, _D, _D], _I),
+    "s2v_copy_out": ([_P, _P, _I, _P], _I),
     "s2v_shard_structure": ([_I64, _I, _I64, _I64, _P, _P, _I64, _P, _P, _P, _P, _P,
                              ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32), _P],
                             _I),

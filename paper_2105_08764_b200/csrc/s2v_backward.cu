@@ -32,6 +32,7 @@ inline int bwd_blocks(const s2v_shard &sh) {
 }
 
 __device__ __forceinline__ int64_t phys_of_row(const s2v_shard &sh, int64_t r) {
+  if (sh.world == 1 && sh.rows_max == sh.num_rows) return r;  // P = 1: identity
   const int64_t b = r / sh.num_rows, i = r - b * sh.num_rows;
   return (b * sh.world + sh.rank) * sh.rows_max + i;
 }
@@ -641,21 +642,23 @@ __global__ void __launch_bounds__(256, 2) layer_backward64_kernel(
 // mT: 8-row group 9 x 16 B) so a warp's staging stores hit 32 distinct banks.
 //
 // Warp roles (640 threads = 5 warps per SM sub-partition at 96 registers,
-// 1 CTA per SM, 32-row tiles, tile = blockIdx.x + i * gridDim.x):
+// 1 CTA per SM, 32-row tiles, tile = blockIdx.x + i * gridDim.x, kStages
+// operand stages):
 //   warps 4-19 (staging): global loads of grad_h / h_l / dzsum / m_l three
 //     tiles ahead in registers (warp = 4 rows x 128 contiguous bytes);
 //     dz = grad_h * (h_l > 0); dzsum += dz to HBM; dzS / dzT / mT hi|lo into
-//     operand stage i % 2; arrive opfull[s]
-//   warp 0, lane 0 (MMA issue, interleaved with its epilogue one tile
-//     behind): 8 + 4 MMAs per tile; commits opfree[s] (stage reusable),
-//     d1full[b] (dm accumulator complete) and, every kDrain tiles, d2full[g]
-//     (dtheta4 group accumulator complete)
+//     operand stage i % kStages; arrive opfull[s]
+//   warp 4, lane 0 (MMA issue, after its staging of the tile): 8 + 4 MMAs
+//     per tile once all staging warps arrived; commits opfree[s] (stage
+//     reusable), d1full[b] (dm accumulator complete) and, every kDrain
+//     tiles, d2full[g] (dtheta4 group accumulator complete)
 //   warps 0-3 (epilogue, TMEM lanes 32 w + [0, 32)): dm^T via tcgen05.ld,
 //     quadrant sums through shared memory, coalesced dm stores; dtheta4
 //     group drains; finally the dtheta4 partial of the CTA.
 // ---------------------------------------------------------------------------
 constexpr int kTR = 32;                       // rows per tile
 constexpr int kTcThreads = 640;               // 20 warps: 5 per SM sub-partition
+constexpr int kStages = 3;                    // operand stages
 constexpr int kDrain = 8;                     // tiles per TMEM dtheta4 group
 constexpr uint32_t kLboS = 65 * 16;           // dzS K-chunk stride
 constexpr uint32_t kSboT = 9 * 16;            // dzT / mT 8-row (M/N) group stride
@@ -665,8 +668,8 @@ constexpr uint32_t kZtBytes = 8 * kLboT;      // 18432
 constexpr uint32_t kThBytes = 32768;          // thT: [k/4][j'/8][8][4]
 constexpr uint32_t kStageBytes = kZsBytes + 2 * kZtBytes;
 constexpr uint32_t kEpiBytes = 32 * 132 * 4;  // dm^T row sums [32 rows][132]
-constexpr uint32_t kAccBytes = 128 * 65 * 4;  // dtheta4 fp32 accumulator [128 k'][65]
-constexpr size_t kTcSmem = 128 + kThBytes + 2 * kStageBytes + kEpiBytes + kAccBytes;
+constexpr uint32_t kAccBytes = 64 * 65 * 4;   // dtheta4 fp32 accumulator [64 k][65]
+constexpr size_t kTcSmem = 128 + kThBytes + kStages * kStageBytes + kEpiBytes + kAccBytes;
 
 __device__ __forceinline__ float tf32_hi(float v) {
   return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
@@ -745,42 +748,46 @@ __global__ void __launch_bounds__(kTcThreads, 1) layer_backward64_tc_kernel(
     const float *__restrict__ h_l, const float *__restrict__ m_l, float *__restrict__ dzsum,
     float *__restrict__ partial, int first, float *__restrict__ dm_out) {
   extern __shared__ uint8_t tc_raw[];
-  uint8_t *base = reinterpret_cast<uint8_t *>(((uintptr_t)tc_raw + 127) & ~(uintptr_t)127);
+  // 128-byte aligned base, derived by pointer arithmetic on the shared array
+  // (not an integer cast) so every access below compiles to STS / LDS
+  uint8_t *base = tc_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(tc_raw) & 127u)) & 127u);
   float *th = reinterpret_cast<float *>(base);
   auto stage_ptr = [&](int s) { return base + kThBytes + (uint32_t)s * kStageBytes; };
-  float *epi = reinterpret_cast<float *>(base + kThBytes + 2 * kStageBytes);  // [32][132]
-  float *acc = epi + kEpiBytes / 4;                                           // [128][65]
-  __shared__ __align__(8) uint64_t bars[12];
+  float *epi = reinterpret_cast<float *>(base + kThBytes + kStages * kStageBytes);  // [32][132]
+  float *acc = epi + kEpiBytes / 4;                                           // [64][65]
+  __shared__ __align__(8) uint64_t bars[2 * kStages + 8];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool want_dm = dm_out != nullptr, want_p4 = m_l != nullptr;
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
   auto opfull = [&](int s) { return bar0 + 8 * s; };
-  auto opfree = [&](int s) { return bar0 + 16 + 8 * s; };
-  auto d1full = [&](int b) { return bar0 + 32 + 8 * b; };
-  auto d1free = [&](int b) { return bar0 + 48 + 8 * b; };
-  auto d2full = [&](int b) { return bar0 + 64 + 8 * b; };
-  auto d2free = [&](int b) { return bar0 + 80 + 8 * b; };
+  auto opfree = [&](int s) { return bar0 + 8 * (kStages + s); };
+  auto d1full = [&](int b) { return bar0 + 8 * (2 * kStages + b); };
+  auto d1free = [&](int b) { return bar0 + 8 * (2 * kStages + 2 + b); };
+  auto d2full = [&](int b) { return bar0 + 8 * (2 * kStages + 4 + b); };
+  auto d2free = [&](int b) { return bar0 + 8 * (2 * kStages + 6 + b); };
   // thT[j'][k]: theta4[k][j' mod 64], hi for j' < 64, lo for j' >= 64
   for (int idx = tid; idx < 128 * 64; idx += kTcThreads) {
     const int jp = idx >> 6, k = idx & 63;
     const float v = theta4[k * 64 + (jp & 63)], h = tf32_hi(v);
     th[((k >> 2) * 16 + (jp >> 3)) * 32 + (jp & 7) * 4 + (k & 3)] = jp < 64 ? h : v - h;
   }
-  for (int idx = tid; idx < 128 * 65; idx += kTcThreads) acc[idx] = 0.f;
+  for (int idx = tid; idx < 64 * 65; idx += kTcThreads) acc[idx] = 0.f;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int s = 0; s < 2; s++) {
+    for (int s = 0; s < kStages; s++) {
       mbar_init(opfull(s), 512);
       mbar_init(opfree(s), 1);
-      mbar_init(d1full(s), 1);
-      mbar_init(d1free(s), 128);
-      mbar_init(d2full(s), 1);
-      mbar_init(d2free(s), 128);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(d1full(b), 1);
+      mbar_init(d1free(b), 128);
+      mbar_init(d2full(b), 1);
+      mbar_init(d2free(b), 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -800,6 +807,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) layer_backward64_tc_kernel(
     const int w = warp - 4;
     const int row = 4 * (w >> 1) + (lane >> 3), c4 = 8 * (w & 1) + (lane & 7);
     const int kc = 4 * c4;  // first k (or j) of the float4
+    const uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | (8u << 17) | (8u << 24);
+    const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | (16u << 17) | (8u << 24);
+    const uint32_t s_th = (uint32_t)__cvta_generic_to_shared(th);
     float4 G[3], H[3], O[3], M[3];
     auto load = [&](int i, float4 &g, float4 &hv, float4 &o, float4 &mv) {
       const int64_t r = tile_row0(i) + row;
@@ -822,7 +832,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) layer_backward64_tc_kernel(
       for (int u = 0; u < 3; u++) {
         const int i = i0 + u;
         if (i >= n_my) break;
-        const int s = i & 1;
+        const int s = u;  // = i % kStages (i0 is a multiple of kStages)
         const int64_t r = tile_row0(i) + row;
         const float4 g = G[u], hv = H[u], o = O[u], mv = M[u];
         float dz[4] = {hv.x > 0.f ? g.x : 0.f, hv.y > 0.f ? g.y : 0.f, hv.z > 0.f ? g.z : 0.f,
@@ -840,7 +850,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) layer_backward64_tc_kernel(
           ml[q] = m4[q] - mh[q];
         }
         load(i + 3, G[u], H[u], O[u], M[u]);  // this set is consumed: refill
-        if (i >= 2) mbar_wait(opfree(s), ((i >> 1) - 1) & 1);
+        if (i >= kStages) mbar_wait(opfree(s), ((i / kStages) - 1) & 1);
         uint8_t *sp = stage_ptr(s);
         float *zs = reinterpret_cast<float *>(sp);
         float *zt = reinterpret_cast<float *>(sp + kZsBytes);
@@ -862,48 +872,45 @@ __global__ void __launch_bounds__(kTcThreads, 1) layer_backward64_tc_kernel(
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(opfull(s));
+        // one staging thread issues the tile's MMAs once every staging warp
+        // has arrived (the epilogue warps never delay the MMA issue; a
+        // dynamic last-arriver issue measured slower: 1.69 vs 1.50 ms)
+        if (warp == 4 && lane == 0) {
+          const int b = i & 1, grp = i / kDrain, gb = grp & 1;
+          const bool g_first = i % kDrain == 0, g_last = i % kDrain == kDrain - 1 || i == n_my - 1;
+          mbar_wait(opfull(s), (i / kStages) & 1);
+          if (i >= 2 && want_dm) mbar_wait(d1free(b), ((i >> 1) - 1) & 1);
+          if (want_p4 && g_first && grp >= 2) mbar_wait(d2free(gb), ((grp >> 1) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t sp = (uint32_t)__cvta_generic_to_shared(stage_ptr(s));
+          const uint32_t s_zs = sp, s_zt = sp + kZsBytes, s_mt = sp + kZsBytes + kZtBytes;
+          if (want_dm) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ks++)  // K = 8 of k per MMA
+              mma_tf32(tmem + 64 * b, umma_desc(s_th + ks * 2 * 2048, 2048, 128),
+                       umma_desc(s_zs + ks * 2 * kLboS, kLboS, 128), idesc1, ks ? 1u : 0u);
+          }
+          if (want_p4) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ks++)  // K = 8 rows per MMA
+              mma_tf32(tmem + 128 + 128 * gb, umma_desc(s_zt + ks * 2 * kLboT, kLboT, kSboT),
+                       umma_desc(s_mt + ks * 2 * kLboT, kLboT, kSboT), idesc2,
+                       (!g_first || ks) ? 1u : 0u);
+          }
+          mma_commit(opfree(s));
+          mma_commit(d1full(b));
+          if (want_p4 && g_last) mma_commit(d2full(gb));
+        }
+        __syncwarp();
       }
     }
   } else {
-    // ---------------- epilogue (warps 0-3: TMEM lanes 32 w + [0, 32)); warp 0
-    // lane 0 also issues the MMAs of tile i before the epilogue of tile i - 1
+    // ---------------- epilogue (warps 0-3: TMEM lanes 32 w + [0, 32)), one
+    // tile behind the MMAs
     const int jp = 32 * warp + lane;  // j' of dm^T, k' of dtheta4
     const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
-    const uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | (8u << 17) | (8u << 24);
-    const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) | (16u << 17) | (8u << 24);
-    const uint32_t s_th = (uint32_t)__cvta_generic_to_shared(th);
 #pragma unroll 1
-    for (int it = 0; it <= n_my; it++) {
-      if (warp == 0 && lane == 0 && it < n_my) {
-        const int i = it;
-        const int s = i & 1, b = i & 1, grp = i / kDrain, gb = grp & 1;
-        const bool g_first = i % kDrain == 0, g_last = i % kDrain == kDrain - 1 || i == n_my - 1;
-        mbar_wait(opfull(s), (i >> 1) & 1);
-        if (i >= 2 && want_dm) mbar_wait(d1free(b), ((i >> 1) - 1) & 1);
-        if (want_p4 && g_first && grp >= 2) mbar_wait(d2free(gb), ((grp >> 1) - 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t sp = (uint32_t)__cvta_generic_to_shared(stage_ptr(s));
-        const uint32_t s_zs = sp, s_zt = sp + kZsBytes, s_mt = sp + kZsBytes + kZtBytes;
-        if (want_dm) {
-#pragma unroll
-          for (int ks = 0; ks < 8; ks++)  // K = 8 of k per MMA
-            mma_tf32(tmem + 64 * b, umma_desc(s_th + ks * 2 * 2048, 2048, 128),
-                     umma_desc(s_zs + ks * 2 * kLboS, kLboS, 128), idesc1, ks ? 1u : 0u);
-        }
-        if (want_p4) {
-#pragma unroll
-          for (int ks = 0; ks < 4; ks++)  // K = 8 rows per MMA
-            mma_tf32(tmem + 128 + 128 * gb, umma_desc(s_zt + ks * 2 * kLboT, kLboT, kSboT),
-                     umma_desc(s_mt + ks * 2 * kLboT, kLboT, kSboT), idesc2,
-                     (!g_first || ks) ? 1u : 0u);
-        }
-        mma_commit(opfree(s));
-        mma_commit(d1full(b));
-        if (want_p4 && g_last) mma_commit(d2full(gb));
-      }
-      __syncwarp();
-      if (it == 0) continue;
-      const int i = it - 1;
+    for (int i = 0; i < n_my; i++) {
       const int b = i & 1, grp = i / kDrain, gb = grp & 1;
       const bool g_last = i % kDrain == kDrain - 1 || i == n_my - 1;
       mbar_wait(d1full(b), (i >> 1) & 1);
@@ -937,13 +944,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) layer_backward64_tc_kernel(
       if (want_p4 && g_last) {  // drain the group's dtheta4 into the fp32 accumulator
         mbar_wait(d2full(gb), (grp >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
+        // u[k'][j] = D2[k'][j] + D2[k'][j + 64]; acc[k][j] += u[k][j], then
+        // += u[k + 64][j]: warps 0-1 (k' < 64) first, warps 2-3 after a
+        // barrier -- a fixed order, so partials are bit-reproducible
 #pragma unroll 1
-        for (int h = 0; h < 2; h++) {
-          float a[32], c[32];
-          tmem_ld32(tmem + lane_base + 128 + 128 * gb + 32 * h, a);
-          tmem_ld32(tmem + lane_base + 128 + 128 * gb + 64 + 32 * h, c);
+        for (int ph = 0; ph < 2; ph++) {
+          if ((warp >> 1) == ph) {
+#pragma unroll 1
+            for (int h = 0; h < 2; h++) {
+              float a[32], c[32];
+              tmem_ld32(tmem + lane_base + 128 + 128 * gb + 32 * h, a);
+              tmem_ld32(tmem + lane_base + 128 + 128 * gb + 64 + 32 * h, c);
 #pragma unroll
-          for (int q = 0; q < 32; q++) acc[jp * 65 + 32 * h + q] += a[q] + c[q];
+              for (int q = 0; q < 32; q++) acc[(jp & 63) * 65 + 32 * h + q] += a[q] + c[q];
+            }
+          }
+          named_sync(2, 128);
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         mbar_arrive(d2free(gb));
@@ -953,9 +969,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) layer_backward64_tc_kernel(
   // ---------------- dtheta4 partial of this CTA: acc[k][j] + acc[k + 64][j]
   __syncthreads();
   for (int idx = tid; idx < 4096; idx += kTcThreads) {
-    const int k = idx >> 6, j = idx & 63;
     float *dst = partial + (int64_t)blockIdx.x * 4096 + idx;
-    *dst = (first ? 0.f : *dst) + (acc[k * 65 + j] + acc[(k + 64) * 65 + j]);
+    *dst = (first ? 0.f : *dst) + acc[(idx >> 6) * 65 + (idx & 63)];
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();

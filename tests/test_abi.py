@@ -49,3 +49,18 @@ def test_status_codes_map_to_reference_exceptions():
 
 def raise_for(code):
     _lib.check(code, "test")
+
+
+def test_library_loads_without_torch():
+    """The C ABI is self-contained: a plain ctypes caller (the reference's
+    own binding) loads libs2v.so and finds the handle-level
+    API without torch in the process."""
+    import subprocess
+    import sys
+    code = ("import ctypes, sys; lib = ctypes.CDLL(%r); "
+            "[getattr(lib, n) for n in ('s2v_ctx_create', 's2v_graph_upload', "
+            "'s2v_state_create', 's2v_embed', 's2v_score_topk', 's2v_apply', 's2v_loss_grad', "
+            "'s2v_adam_update', 's2v_copy_out')]; assert 'torch' not in sys.modules; "
+            "print('ok')" % str(_lib.LIB_PATH))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr
