@@ -1260,10 +1260,40 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
           (float *)h_out, (float *)m_out, hub_counter, hot_rows, peers, npeers, deg_src);
     }, &ss);
     if (rc) return rc;
+    // experiment hook: an L2 persisting window over the lowest rows of h_in
+    // (cudaLimitPersistingL2CacheSize + stream access policy), S2V_L2_PERSIST_MB
+    static const int persist_mb = [] {
+      const char *e = getenv("S2V_L2_PERSIST_MB");
+      return e ? atoi(e) : 0;
+    }();
+    const bool persist = persist_mb > 0 && h_in && !from_table;
+    if (persist) {
+      static bool limit_set = false;
+      if (!limit_set) {
+        int dev = 0, maxp = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
+                           std::min<size_t>((size_t)persist_mb << 20, (size_t)maxp));
+        limit_set = true;
+      }
+      cudaStreamAttrValue v = {};
+      v.accessPolicyWindow.base_ptr = const_cast<void *>(h_in);
+      v.accessPolicyWindow.num_bytes = (size_t)persist_mb << 20;
+      v.accessPolicyWindow.hitRatio = 1.0f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      S2V_CUDA_CHECK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v));
+    }
     kern<<<grid, 256, 0, st>>>(*sh, (const float *)theta4, (const float *)table, max_deg,
                                (const float *)h_in, (float *)h_out, (float *)m_out, counter,
                                hot_rows, peers, npeers, deg_src);
     S2V_LAUNCH_CHECK();
+    if (persist) {
+      cudaStreamAttrValue v = {};
+      v.accessPolicyWindow.num_bytes = 0;
+      S2V_CUDA_CHECK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v));
+    }
     if (ss) S2V_CUDA_CHECK(cudaStreamWaitEvent(st, ss->done, 0));
     S2V_LAUNCH_CHECK();
     return S2V_OK;
