@@ -72,7 +72,8 @@ typedef struct {
                               rows (degree > S2V_HUB_DEGREE) first, then the
                               rest, each by descending degree; NULL = identity */
   int64_t n_hub;           /* rows handled by the CTA-cooperative hub kernel */
-  const int32_t *active;   /* NULL, or the active-row list (B = 1, P = 1): a
+  const int32_t *active;   /* NULL, or the active-row list (B = 1; local rows,
+                              any P; the compact CSR below only at P = 1): a
                               stable subsequence of `order` holding every row
                               with rdeg > 0 (s2v_active_compact); the
                               forward rounds and the scorer then visit only
@@ -189,7 +190,7 @@ int s2v_trow(const s2v_shard *sh, int max_deg, int32_t *trow_phys, void *stream)
  * active_cols.  `cap` bounds n[0] (host-side capacity of
  * list, tmp); ws holds s2v_active_workspace(cap) int64.  The rows dropped
  * never come back: a residual degree only decreases during an episode
- * (state.py:173-208).  B = 1, P = 1. */
+ * (state.py:173-208).  B = 1; the compact CSR outputs only at P = 1. */
 int s2v_active_compact(const s2v_shard *sh, int32_t *list, int64_t *n, int32_t *tmp,
                        int64_t *ws, int64_t cap, int64_t *row_ptr_out, uint32_t *cols_out,
                        void *stream);
@@ -228,9 +229,13 @@ size_t s2v_colsum_workspace(const s2v_shard *sh, int K, int elem_bytes);
 int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
                         const void *h1_table, int max_deg, void *g, void *workspace,
                         size_t workspace_bytes, uint8_t *last, int full,
-                        const int32_t *dirty_rows, const int64_t *ndirty, void *stream);
-/* (dirty_rows, ndirty: incremental forward -- only the leaves holding one of
- * these rows (every row whose embedding changed) are recomputed.)  Workspace
+                        const int32_t *dirty_rows, const int64_t *ndirty,
+                        const int32_t *trow_phys, void *stream);
+/* (dirty_rows, ndirty: incremental forward, P = 1 -- only the leaves holding
+ * one of these rows (every row whose embedding changed) are recomputed.
+ * trow_phys: P > 1 (NULL at P = 1) -- every rank's e12 table row by physical
+ * row (s2v_trow + the all-gather of round 2), which classifies every node of
+ * the gathered buffer: 0 dead, max_deg + 1 in S, else alive.)  Workspace
  * bytes for s2v_colsum_residual: */
 size_t s2v_colsum_residual_workspace(const s2v_shard *sh, int K, int elem_bytes);
 

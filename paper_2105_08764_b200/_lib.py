@@ -85,7 +85,7 @@ _SIGNATURES = {
     "s2v_embed_round_peers": ([_I, _SH, _P, _P, _I, _I, _P, _P, _P, _I, _P, _P], _I),
     "s2v_colsum": ([_I, _SH, _I, _P, _P, _P, _SZ, _P], _I),
     "s2v_colsum_workspace": ([_SH, _I, _I], _SZ),
-    "s2v_colsum_residual": ([_I, _SH, _I, _P, _P, _I, _P, _P, _SZ, _P, _I, _P, _P, _P], _I),
+    "s2v_colsum_residual": ([_I, _SH, _I, _P, _P, _I, _P, _P, _SZ, _P, _I, _P, _P, _P, _P], _I),
     "s2v_colsum_residual_workspace": ([_SH, _I, _I], _SZ),
     "s2v_score_cached": ([_SH, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P], _I),
     "s2v_frontier_seed": ([_SH, _P, _I, _I, _P, _P, _P, _I64, _P], _I),

@@ -401,10 +401,15 @@ struct PairwiseCtx {
   const void *h;
   int64_t N, rows_max, base, extra;
   int32_t P, b, K;
-  // residual mode (P = 1): rows with rdeg = 0 read dead[sol ? K : 0 .. + K)
+  // residual mode: rows with rdeg = 0 read dead[sol ? K : 0 .. + K).  P = 1
+  // classifies from the shard's rdeg / sol; P > 1 from trow, every rank's
+  // e12 table row by physical row (s2v_trow + the round-2 exchange):
+  // 0 = rdeg 0 outside S, max_deg + 1 = in S, anything else alive
   const void *dead;
   const int32_t *rdeg;
   const uint8_t *sol;
+  const int32_t *trow;
+  int32_t max_deg;
   // incremental residual mode: last[row] = the row's class at the previous
   // call (0 live, 1/2 dead); a leaf dead now and then keeps its value
   uint8_t *last;
@@ -413,6 +418,18 @@ struct PairwiseCtx {
   // are recomputed, the rest keep their cached sums
   const uint8_t *leaf_dirty;
 };
+
+__device__ __forceinline__ int64_t phys_node(const PairwiseCtx &c, int64_t u);
+
+// residual class of global node u of slot c.b: 0 alive, 1 dead (sol 0), 2 in S
+__device__ __forceinline__ uint8_t dead_code(const PairwiseCtx &c, int64_t u) {
+  if (c.trow) {
+    const int32_t t = c.trow[phys_node(c, u)];
+    return t == 0 ? 1 : (t == c.max_deg + 1 ? 2 : 0);
+  }
+  const int64_t r = (int64_t)c.b * c.N + u;
+  return c.rdeg[r] == 0 ? (c.sol[r] ? 2 : 1) : 0;
+}
 
 __device__ __forceinline__ int64_t phys_node(const PairwiseCtx &c, int64_t u) {
   if (c.P == 1) return (int64_t)c.b * c.rows_max + u;
@@ -425,8 +442,8 @@ __device__ __forceinline__ int64_t phys_node(const PairwiseCtx &c, int64_t u) {
 template <class T>
 __device__ __forceinline__ T load_node(const PairwiseCtx &c, int64_t u, int k) {
   if (c.dead) {
-    const int64_t r = (int64_t)c.b * c.N + u;
-    if (c.rdeg[r] == 0) return reinterpret_cast<const T *>(c.dead)[(c.sol[r] ? c.K : 0) + k];
+    const uint8_t code = dead_code(c, u);
+    if (code) return reinterpret_cast<const T *>(c.dead)[(code - 1) * c.K + k];
   }
   int64_t phys;
   if (c.P == 1) {
@@ -496,7 +513,7 @@ __global__ void __launch_bounds__(512) colsum_leaf64_kernel(PairwiseCtx c,
     bool live = false;
     if (tid < n) {
       const int64_t r = (int64_t)c.b * c.N + u0 + tid;
-      const uint8_t code = c.rdeg[r] == 0 ? (c.sol[r] ? 2 : 1) : 0;
+      const uint8_t code = dead_code(c, u0 + tid);
       s_code[tid] = code;
       live = code == 0;
       if (c.last) {  // a row only ever goes live -> dead (rdeg never grows)
@@ -584,7 +601,7 @@ __global__ void __launch_bounds__(256) colsum_leaf64x4_kernel(PairwiseCtx c,
       const int i = k + 64 * h2;
       if (i < n) {
         const int64_t r = (int64_t)c.b * c.N + u0 + i;
-        const uint8_t code = c.rdeg[r] == 0 ? (c.sol[r] ? 2 : 1) : 0;
+        const uint8_t code = dead_code(c, u0 + i);
         s_code[ll][i] = code;
         live |= code == 0;
         if (c.last) {  // a row only ever goes live -> dead (rdeg never grows)
@@ -777,7 +794,8 @@ template <class T>
 static int colsum_t(const s2v_shard *sh, int K, const void *h, void *g, void *workspace,
                     size_t workspace_bytes, cudaStream_t st, const T *dead = nullptr,
                     uint8_t *last = nullptr, int full = 1, const int32_t *dirty_rows = nullptr,
-                    const int64_t *ndirty = nullptr, uint8_t *flags = nullptr) {
+                    const int64_t *ndirty = nullptr, uint8_t *flags = nullptr,
+                    const int32_t *trow = nullptr, int max_deg = 0) {
   PairwisePlan *plan = nullptr;
   int rc = get_plan(sh->num_nodes, &plan);
   if (rc) return rc;
@@ -797,6 +815,8 @@ static int colsum_t(const s2v_shard *sh, int K, const void *h, void *g, void *wo
   c.dead = dead;
   c.rdeg = sh->rdeg;
   c.sol = sh->sol;
+  c.trow = trow;
+  c.max_deg = max_deg;
   c.last = last;
   c.full = full;
   c.leaf_dirty = nullptr;
@@ -1231,8 +1251,9 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
     return fail(S2V_EINVAL, "degree-table rounds need K = 64 fp32 (and every rank's degrees "
                             "at P > 1)");
   const int32_t *deg_src = deg_phys ? deg_phys : sh->rdeg;
-  if (sh->active && !(sizeof(T) == 4 && K == 64 && sh->world == 1 && sh->batch == 1))
-    return fail(S2V_EINVAL, "active-row lists need K = 64 fp32, B = 1, P = 1");
+  if (sh->active && !(sizeof(T) == 4 && K == 64 && sh->batch == 1 &&
+                      (sh->world == 1 || !sh->active_ptr)))
+    return fail(S2V_EINVAL, "active-row lists need K = 64 fp32, B = 1 (compact CSR: P = 1)");
   if (sizeof(T) == 4 && K == 64) {
     static thread_local int *counter = nullptr;
     if (!counter) S2V_CUDA_CHECK(cudaMalloc(&counter, sizeof(int)));
@@ -1241,7 +1262,9 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
     int grid = (int)std::min<int64_t>(ntiles, kNumSMs * 4);
     // rows kept in L2 with evict_last: the lowest physical ids -- the BA hubs,
     // 48 MB of rows source 31% of all gathers at BA(2M,16) (measured best of
-    // 0/48/80/110 MB; S2V_HOT_MB overrides)
+    // 0/48/80/110 MB; S2V_HOT_MB overrides).  A persisting L2 carve-out
+    // (cudaLimitPersistingL2CacheSize + access-policy window of 48/80/100 MB)
+    // measured no better with these hints and worse without.
     uint32_t hot_rows;
     static const uint32_t hot_env = [] {
       const char *e = getenv("S2V_HOT_MB");
@@ -1260,40 +1283,10 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
           (float *)h_out, (float *)m_out, hub_counter, hot_rows, peers, npeers, deg_src);
     }, &ss);
     if (rc) return rc;
-    // experiment hook: an L2 persisting window over the lowest rows of h_in
-    // (cudaLimitPersistingL2CacheSize + stream access policy), S2V_L2_PERSIST_MB
-    static const int persist_mb = [] {
-      const char *e = getenv("S2V_L2_PERSIST_MB");
-      return e ? atoi(e) : 0;
-    }();
-    const bool persist = persist_mb > 0 && h_in && !from_table;
-    if (persist) {
-      static bool limit_set = false;
-      if (!limit_set) {
-        int dev = 0, maxp = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
-                           std::min<size_t>((size_t)persist_mb << 20, (size_t)maxp));
-        limit_set = true;
-      }
-      cudaStreamAttrValue v = {};
-      v.accessPolicyWindow.base_ptr = const_cast<void *>(h_in);
-      v.accessPolicyWindow.num_bytes = (size_t)persist_mb << 20;
-      v.accessPolicyWindow.hitRatio = 1.0f;
-      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      S2V_CUDA_CHECK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v));
-    }
     kern<<<grid, 256, 0, st>>>(*sh, (const float *)theta4, (const float *)table, max_deg,
                                (const float *)h_in, (float *)h_out, (float *)m_out, counter,
                                hot_rows, peers, npeers, deg_src);
     S2V_LAUNCH_CHECK();
-    if (persist) {
-      cudaStreamAttrValue v = {};
-      v.accessPolicyWindow.num_bytes = 0;
-      S2V_CUDA_CHECK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v));
-    }
     if (ss) S2V_CUDA_CHECK(cudaStreamWaitEvent(st, ss->done, 0));
     S2V_LAUNCH_CHECK();
     return S2V_OK;
@@ -1494,8 +1487,12 @@ size_t s2v_colsum_residual_workspace(const s2v_shard *sh, int K, int elem_bytes)
 int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
                         const void *h1_table, int max_deg, void *g, void *workspace,
                         size_t workspace_bytes, uint8_t *last, int full,
-                        const int32_t *dirty_rows, const int64_t *ndirty, void *stream) {
-  if (sh->world != 1) return fail(S2V_EINVAL, "residual colsum needs P = 1");
+                        const int32_t *dirty_rows, const int64_t *ndirty,
+                        const int32_t *trow_phys, void *stream) {
+  if (sh->world != 1 && !trow_phys)
+    return fail(S2V_EINVAL, "residual colsum at P > 1 needs every rank's e12 rows (trow)");
+  if (sh->world != 1 && dirty_rows)
+    return fail(S2V_EINVAL, "dirty-row colsum needs P = 1");
   if (max_deg < 0 || !h1_table) return fail(S2V_EINVAL, "bad residual colsum args");
   cudaStream_t st = as_stream(stream);
   const size_t elem = dt == S2V_F32 ? 4 : 8;
@@ -1508,13 +1505,13 @@ int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
     dead_rows_kernel<float><<<1, 64, 0, st>>>((const float *)h1_table, K, max_deg, (float *)dead);
     S2V_LAUNCH_CHECK();
     return colsum_t<float>(sh, K, h, g, workspace, need, st, (const float *)dead, last, full,
-                           dirty_rows, ndirty, flags);
+                           dirty_rows, ndirty, flags, sh->world > 1 ? trow_phys : nullptr, max_deg);
   }
   dead_rows_kernel<double><<<1, 64, 0, st>>>((const double *)h1_table, K, max_deg,
                                              (double *)dead);
   S2V_LAUNCH_CHECK();
   return colsum_t<double>(sh, K, h, g, workspace, need, st, (const double *)dead, last, full,
-                          dirty_rows, ndirty, flags);
+                          dirty_rows, ndirty, flags, sh->world > 1 ? trow_phys : nullptr, max_deg);
 }
 
 int s2v_score_blocks(const s2v_shard *sh) {
@@ -1528,8 +1525,8 @@ int s2v_score(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, const voi
               const void *theta6, const void *theta7, const uint8_t *cand_override, int mode,
               void *scores, uint64_t *block_keys, int64_t *counts, void *stream) {
   if (K > 256) return fail(S2V_EINVAL, "embed_dim %d > 256 unsupported", K);
-  if (sh->active && !(dt == S2V_F32 && K == 64 && sh->world == 1 && sh->batch == 1))
-    return fail(S2V_EINVAL, "active-row lists need K = 64 fp32, B = 1, P = 1");
+  if (sh->active && !(dt == S2V_F32 && K == 64 && sh->batch == 1))
+    return fail(S2V_EINVAL, "active-row lists need K = 64 fp32, B = 1");
   cudaStream_t st = as_stream(stream);
   S2V_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(int64_t) * sh->batch, st));
   dim3 grid(s2v_score_blocks(sh), sh->batch);

@@ -465,8 +465,9 @@ int64_t s2v_active_workspace(int64_t cap) {
 int s2v_active_compact(const s2v_shard *sh, int32_t *list, int64_t *n, int32_t *tmp,
                        int64_t *ws, int64_t cap, int64_t *row_ptr_out, uint32_t *cols_out,
                        void *stream) {
-  if (sh->batch != 1 || sh->world != 1)
-    return fail(S2V_EINVAL, "active-row lists need B = 1, P = 1");
+  // (the list holds local rows: any P; the compact CSR is read only at P = 1)
+  if (sh->batch != 1 || (sh->world != 1 && cols_out))
+    return fail(S2V_EINVAL, "active-row lists need B = 1 (compact CSR: P = 1)");
   if ((row_ptr_out == nullptr) != (cols_out == nullptr))
     return fail(S2V_EINVAL, "compact CSR needs both row_ptr_out and cols_out");
   if (cap <= 0) return S2V_OK;

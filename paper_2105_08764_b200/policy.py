@@ -319,7 +319,7 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
             _lib.call("s2v_h1_table", dt, dparams.ptr("theta4"), ptr(table), k, max_deg,
                       ptr(h1t), st)
     elif state.active_on:
-        raise RuntimeError("active-row lists need the degree-table round (K = 64 fp32, P = 1)")
+        raise RuntimeError("active-row lists need the degree-table round (K = 64 fp32)")
     state._tables_of = dparams
     sh = state.shard
     outer = (sh.active, sh.active_n, sh.active_ptr, sh.active_cols)
@@ -424,11 +424,14 @@ def _colsum_device(emb: DeviceEmbedding) -> torch.Tensor:
         # take their (constant) round-1 row from the h1 table; an episode
         # keeps its own tree workspace so that all-dead leaves are reused
         h1t = st.workspace("h1t", (k, int(st.max_deg)), None)
+        # P > 1: every rank's e12 rows by physical row, exchanged by this
+        # forward's round 2, classify the gathered buffer's rows
+        trow = st._ws["trow"][1] if st.world > 1 else None
         inc = st.colsum_cache
         if inc is None:
             _lib.call("s2v_colsum_residual", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h),
                       ptr(h1t), int(st.max_deg), ptr(ws["g"]), ptr(ws["ws"]), wsb, None, 1,
-                      None, None, stream_ptr())
+                      None, None, ptr(trow), stream_ptr())
         else:
             if inc.get("ws") is None:
                 inc["ws"] = torch.empty_like(ws["ws"])
@@ -439,7 +442,7 @@ def _colsum_device(emb: DeviceEmbedding) -> torch.Tensor:
             _lib.call("s2v_colsum_residual", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h),
                       ptr(h1t), int(st.max_deg), ptr(ws["g"]), ptr(inc["ws"]), wsb,
                       ptr(inc["last"]), 1 if inc["full"] else 0, dirty[0], dirty[1],
-                      stream_ptr())
+                      ptr(trow), stream_ptr())
             inc["full"] = False
     else:
         _lib.call("s2v_colsum", _dt_code(emb.dtype), st.shard_ref(), k, ptr(emb.h),

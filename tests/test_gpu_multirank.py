@@ -155,3 +155,40 @@ def test_device_tau_loop_at_p_ranks(p):
         assert losses == outs[0][0]
         for k in P.PARAM_NAMES:
             assert np.array_equal(getattr(params, k), getattr(outs[0][1], k))
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_compacted_episode_at_p_ranks(p, monkeypatch):
+    """Residual-row compaction at P > 1 (every rank visits only its rows with
+    rdeg > 0; the gathered global sum takes dead rows from the h1 table,
+    classified by every rank's e12 rows): the whole episode's pick/apply
+    trace equals the P = 1 loop over every row.  R-MAT with isolated nodes."""
+    from paper_2105_08764_b200.inference import DeviceEpisode
+    monkeypatch.setattr(DeviceEpisode, "COMPACT_MIN_ROWS", 0)
+    g = P.generate_rmat(13, 16, 2)
+    params = P.PolicyParams.initialize(64, 5, seed=6)
+    sched = P.SelectionSchedule.adaptive()
+
+    def run(compact):
+        def worker(comm):
+            st = P.PartitionedState([g], P.partition_rows(g.num_nodes, comm.size)[comm.rank])
+            ep = DeviceEpisode(st, params, comm, sched, 4, use_graph=False, compact=compact)
+            assert ep.compact == compact
+            trace = []
+            while True:
+                tp, ta, te, active = ep.run_chunk()
+                trace.append((tp.copy(), ta.copy(), te.copy()))
+                if not active.any():
+                    break
+            return trace, ep.active_count()
+        return P.run_workers(comm_size[0], worker)
+
+    comm_size = [1]
+    (t_f, _), = run(False)
+    comm_size[0] = p
+    outs = run(True)
+    for trace, n_act in outs:
+        assert len(trace) == len(t_f)
+        for (a, b, c), (x, y, z) in zip(trace, t_f):
+            assert np.array_equal(a, x) and np.array_equal(b, y) and np.array_equal(c, z)
+        assert n_act < g.num_nodes // p + 1  # the list did shrink
