@@ -192,3 +192,36 @@ def test_compacted_episode_at_p_ranks(p, monkeypatch):
         for (a, b, c), (x, y, z) in zip(trace, t_f):
             assert np.array_equal(a, x) and np.array_equal(b, y) and np.array_equal(c, z)
         assert n_act < g.num_nodes // p + 1  # the list did shrink
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_d1_schedule_is_stepwise_argmax_at_p_ranks(p):
+    """The reference's equivalence (pkg/tests/test_inference.py:84-110) at
+    P ranks: the d = 1 schedule through solve() (the device episode loop,
+    keys merged across ranks) picks exactly the stepwise argmax of the
+    all-gathered masked scores (env.step through the public API), on a
+    BA graph large enough that every rank owns hubs and leaves."""
+    g = P.generate_ba(600, 3, 21)
+    params = P.PolicyParams.initialize(16, 3, seed=3)
+
+    def manual(comm):
+        env = P.reset(g, comm)
+        picks = []
+        while not env.terminated:
+            emb = P.embed_forward(env.state, params, comm)
+            sc = P.q_forward(emb, env.state.cand, params, comm)
+            gl = comm.all_gather(P.masked_scores(sc, env.state.cand), axis=-1)[0]
+            v = int(np.argmax(gl))
+            env.step(v)
+            picks.append(v)
+        return picks
+
+    def via_solve(comm):
+        (res,) = P.solve([g], params, comm, schedule=P.SelectionSchedule.single())
+        return res
+    picks = P.run_workers(p, manual)
+    res = P.run_workers(p, via_solve)
+    for pk, r in zip(picks, res):
+        assert pk == picks[0]
+        assert r.cover == sorted(pk)
+        assert r.policy_evals == len(pk)
