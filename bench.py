@@ -707,8 +707,16 @@ def main():
         sol_host[0, part.row_start:part.row_stop] = state.sol[0]
         if world > 1:
             sol_host[0] = comm.all_reduce_sum(sol_host[0], tag="bench")
+        held = []
+
         def e2e_step():
+            # the caller drops the previous step's state before building the
+            # next (its device buffers go back to the caching allocator now,
+            # not whenever Python's cycle collector runs)
+            while held:
+                held.pop().release()
             st2 = P.PartitionedState([graph], part, solutions=sol_host)
+            held.append(st2)
             picks, applied = solve_step(st2, params, comm, sched, active)
             for v, a in zip(picks[0], applied[0]):
                 if v >= 0 and a:

@@ -100,8 +100,11 @@ int s2v_set_device(int device);
 /* ---- state (pkg/src/graphrl/state.py) ----------------------------------- */
 /* Mark dead entries, compute rdeg/sol/cand/residual from a solution vector
  * indexed by physical row (sol_phys[B*P*rows_max]).  Replaces the residual
- * mask + row sums of PartitionedState.__init__ (state.py:89-111). */
-int s2v_shard_init(const s2v_shard *sh, const uint8_t *sol_phys, void *stream);
+ * mask + row sums of PartitionedState.__init__ (state.py:89-111).
+ * cols_src (nullable): the cached read-only column array of the graph's
+ * structure, copied into sh->cols with the dead bits in the same pass. */
+int s2v_shard_init(const s2v_shard *sh, const uint32_t *cols_src, const uint8_t *sol_phys,
+                   void *stream);
 
 /* Block-diagonal batch assembly (PartitionedState over B graphs): for each
  * segment, dst[dst_off + i] = src[i] + add, i < len, on 4- or 8-byte

@@ -73,7 +73,7 @@ _SIGNATURES = {
     "s2v_last_error": ([], ctypes.c_char_p),
     "s2v_version": ([], ctypes.c_char_p),
     "s2v_set_device": ([_I], _I),
-    "s2v_shard_init": ([_SH, _P, _P], _I),
+    "s2v_shard_init": ([_SH, _P, _P, _P], _I),
     "s2v_segment_copy": ([_I, _P, _I, _I64, _P, _P], _I),
     "s2v_apply_phase1": ([_SH, _P, _I, _P, _I, _P, _P], _I),
     "s2v_apply_phase2": ([_SH, _P, _I, _P, _P, _P, _I, _P], _I),
@@ -207,7 +207,7 @@ def check(rc: int, what: str = "") -> None:
 
 # kernels each entry point launches (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {
-    "s2v_shard_init": 1, "s2v_apply_phase1": 1, "s2v_apply_phase2": 2, "s2v_e12_table": 1,
+    "s2v_shard_init": 2, "s2v_apply_phase1": 1, "s2v_apply_phase2": 2, "s2v_e12_table": 1,
     "s2v_embed_round": 1, "s2v_embed_round_peers": 1, "s2v_colsum": 2, "s2v_score": 1, "s2v_topk_merge": 1, "s2v_score_keys": 1, "s2v_score_keys_f64": 1,
     "s2v_topk_below": 1,
     "s2v_grad_h_init": 1, "s2v_layer_backward": 1, "s2v_gather": 1, "s2v_param_grads": 1,

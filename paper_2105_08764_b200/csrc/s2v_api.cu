@@ -384,7 +384,7 @@ int s2v_state_create(s2v_ctx *ctx, s2v_graph *const *graphs, int B, const uint8_
     delete st;
     return fail(S2V_ECUDA, "state create: solution upload failed");
   }
-  rc = s2v_shard_init(&sh, sol_d, ctx->stream);
+  rc = s2v_shard_init(&sh, nullptr, sol_d, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   cudaFree(sol_d);
   if (rc) {

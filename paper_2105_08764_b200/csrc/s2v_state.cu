@@ -54,37 +54,79 @@ __device__ __forceinline__ int64_t phys_of(const s2v_shard &sh, const PartitionM
   return ((int64_t)b * sh.world + r) * sh.rows_max + (u - pm.start(r));
 }
 
-// One warp per local row: entry alive iff neither endpoint is in S.
-__global__ void shard_init_kernel(s2v_shard sh, const uint8_t *__restrict__ sol_phys) {
-  const int lane = threadIdx.x & 31;
+// Entry alive iff neither endpoint is in S.  Eight lanes per local row
+// (four rows per warp in flight: a BA row of ~32 entries is 4 steps, and the
+// row_ptr -> cols -> sol[nbr] chain of each row overlaps three others);
+// cols_src (nullable) is the read-only structure's column array, copied into
+// sh.cols with the dead bits in the same pass (no separate clone).
+// sol bytes -> bitmap (1 bit per physical row): the neighbour test of
+// shard_init_kernel then reads a 256 KB (BA(2M,16)) array that stays in L1
+__global__ void sol_bits_kernel(const uint8_t *__restrict__ sol_phys, int64_t n,
+                                uint32_t *__restrict__ bits) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < (n + 31) / 32;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    for (int j = 0; j < 32 && 32 * w + j < n; j++) v |= (sol_phys[32 * w + j] ? 1u : 0u) << j;
+    bits[w] = v;
+  }
+}
+
+__global__ void shard_init_kernel(s2v_shard sh, const uint32_t *__restrict__ cols_src,
+                                  const uint8_t *__restrict__ sol_phys,
+                                  const uint32_t *__restrict__ sol_bits) {
+  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
+  const uint32_t *src = cols_src ? cols_src : sh.cols;
   // per-warp running count of alive entries, flushed once per slot (one
   // atomic per warp and slot instead of one per row)
   int64_t acc_b = -1;
   unsigned long long acc = 0;
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < nrows;
-       r += (gridDim.x * (int64_t)blockDim.x) >> 5) {
-    const int64_t b = r / sh.num_rows, i = r - b * sh.num_rows;
-    if (b != acc_b) {
-      if (lane == 0 && acc) atomicAdd((unsigned long long *)&sh.residual[acc_b], acc);
-      acc_b = b;
-      acc = 0;
+  const int64_t wstride = ((gridDim.x * (int64_t)blockDim.x) >> 5) * 4;
+  for (int64_t w0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 4; w0 < nrows;
+       w0 += wstride) {  // warp-uniform loop: rows w0 + grp
+    const int64_t r = w0 + grp;
+    const bool ok = r < nrows;
+    int64_t b = 0, i = r;
+    if (ok && sh.batch > 1) {
+      b = r / sh.num_rows;
+      i = r - b * sh.num_rows;
     }
-    const uint8_t s = sol_phys[(b * sh.world + sh.rank) * sh.rows_max + i];
+    uint8_t s = 0;
     int cnt = 0;
-    for (int64_t e = sh.row_ptr[r] + lane; e < sh.row_ptr[r + 1]; e += 32) {
-      uint32_t c = sh.cols[e] & ~S2V_DEAD;
-      bool dead = s || sol_phys[c];
-      sh.cols[e] = c | (dead ? S2V_DEAD : 0u);
-      cnt += !dead;
+    if (ok) {
+      s = sol_phys[(b * sh.world + sh.rank) * sh.rows_max + i];
+      const int64_t e1 = sh.row_ptr[r + 1];
+      for (int64_t e = sh.row_ptr[r] + sub; e < e1; e += 8) {
+        const uint32_t c = src[e] & ~S2V_DEAD;
+        const bool dead = s || ((__ldg(sol_bits + (c >> 5)) >> (c & 31)) & 1u);
+        sh.cols[e] = c | (dead ? S2V_DEAD : 0u);
+        cnt += !dead;
+      }
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) {
+    for (int o = 4; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (ok && sub == 0) {
       sh.rdeg[r] = cnt;
       sh.sol[r] = s;
       sh.cand[r] = (cnt > 0 && !s) ? 1 : 0;
-      acc += (unsigned long long)cnt;
+    }
+    // slot counts: the warp's rows share a slot unless a slot boundary
+    // falls inside the 4 rows (then per-row atomics)
+    const int64_t b0 = __shfl_sync(0xffffffffu, b, 0);
+    if (__all_sync(0xffffffffu, !ok || b == b0)) {
+      unsigned long long c4 = (ok && sub == 0) ? (unsigned long long)cnt : 0ull;
+      c4 += __shfl_xor_sync(0xffffffffu, c4, 8);
+      c4 += __shfl_xor_sync(0xffffffffu, c4, 16);
+      if (lane == 0) {
+        if (b0 != acc_b) {
+          if (acc) atomicAdd((unsigned long long *)&sh.residual[acc_b], acc);
+          acc_b = b0;
+          acc = 0;
+        }
+        acc += c4;
+      }
+    } else if (ok && sub == 0 && cnt) {
+      atomicAdd((unsigned long long *)&sh.residual[b], (unsigned long long)cnt);
     }
   }
   if (lane == 0 && acc) atomicAdd((unsigned long long *)&sh.residual[acc_b], acc);
@@ -421,16 +463,24 @@ int s2v_set_device(int device) {
   return S2V_OK;
 }
 
-int s2v_shard_init(const s2v_shard *sh, const uint8_t *sol_phys, void *stream) {
+int s2v_shard_init(const s2v_shard *sh, const uint32_t *cols_src, const uint8_t *sol_phys,
+                   void *stream) {
   if (!sh || sh->batch < 1 || sh->world < 1) return fail(S2V_EINVAL, "bad shard");
   cudaStream_t st = as_stream(stream);
   S2V_CUDA_CHECK(cudaMemsetAsync(sh->residual, 0, sizeof(int64_t) * sh->batch, st));
   int64_t rows = (int64_t)sh->batch * sh->num_rows;
   if (rows == 0) return S2V_OK;
-  int64_t blocks = (rows * 32 + 255) / 256;
-  if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
-  shard_init_kernel<<<(unsigned)blocks, 256, 0, st>>>(*sh, sol_phys);
+  const int64_t nphys = (int64_t)sh->batch * sh->world * sh->rows_max;
+  uint32_t *bits = nullptr;
+  S2V_CUDA_CHECK(cudaMallocAsync((void **)&bits, 4 * ((nphys + 31) / 32), st));
+  sol_bits_kernel<<<(unsigned)std::min<int64_t>(((nphys + 31) / 32 + 255) / 256, kNumSMs * 8),
+                    256, 0, st>>>(sol_phys, nphys, bits);
   S2V_LAUNCH_CHECK();
+  int64_t blocks = (rows * 8 + 255) / 256;
+  if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+  shard_init_kernel<<<(unsigned)blocks, 256, 0, st>>>(*sh, cols_src, sol_phys, bits);
+  S2V_LAUNCH_CHECK();
+  S2V_CUDA_CHECK(cudaFreeAsync(bits, st));
   return S2V_OK;
 }
 

@@ -180,15 +180,18 @@ class PartitionedState:
         slot_stride = P * self.rows_max
         if batch == 1 and self.nnz:
             # one slot: the cached read-only structure is used in place; only
-            # the column array (which carries the removed-edge bits) is copied
+            # the column array (which carries the removed-edge bits) is a
+            # copy, written by s2v_shard_init from the structure's
             s0 = structs[0]
             self.row_ptr, self.col_ptr, self.col_ent, self.col_row = (
                 s0.row_ptr, s0.col_ptr, s0.col_ent, s0.col_row)
-            self.cols = s0.cols0.clone()
+            self.cols = torch.empty_like(s0.cols0)
+            cols_src = s0.cols0
             self.order = s0.order if rows else torch.zeros(1, dtype=torch.int32, device=dev)
         else:
             # block-diagonal assembly over slots (device-to-device, structure
             # cached): one segment-copy launch per array
+            cols_src = None
             e = [int(x) for x in ent_off]
             lp = int(structs[0].col_ptr.numel())
             self.row_ptr = _assemble(dev, torch.int64, batch * rows + 1, [
@@ -221,10 +224,13 @@ class PartitionedState:
                 self.order = torch.zeros(1, dtype=torch.int32, device=dev)
         self.n_hub = sum(s.n_hub for s in structs)
         nr = max(batch * rows, 1)
-        self.rdeg = torch.zeros(nr, dtype=torch.int32, device=dev)
-        self.sol_d = torch.zeros(nr, dtype=torch.uint8, device=dev)
-        self.cand_d = torch.zeros(nr, dtype=torch.uint8, device=dev)
-        self.residual_d = torch.zeros(batch, dtype=torch.int64, device=dev)
+        # every row's rdeg / sol / cand and the residual counts are written by
+        # s2v_shard_init (no fill launches)
+        alloc = torch.empty if rows else torch.zeros
+        self.rdeg = alloc(nr, dtype=torch.int32, device=dev)
+        self.sol_d = alloc(nr, dtype=torch.uint8, device=dev)
+        self.cand_d = alloc(nr, dtype=torch.uint8, device=dev)
+        self.residual_d = torch.empty(batch, dtype=torch.int64, device=dev)
         self._shard = _lib.s2v_shard(
             num_nodes=n, batch=batch, world=P, rank=part.rank, _pad=0,
             row_start=part.row_start, num_rows=rows, rows_max=self.rows_max, nnz=self.nnz,
@@ -232,14 +238,15 @@ class PartitionedState:
             col_ent=ptr(self.col_ent), col_row=ptr(self.col_row), rdeg=ptr(self.rdeg),
             sol=ptr(self.sol_d), cand=ptr(self.cand_d), residual=ptr(self.residual_d),
             order=ptr(self.order), n_hub=self.n_hub)
-        sol_phys = np.zeros((batch, P, self.rows_max), dtype=np.uint8)
-        if P == 1:
-            sol_phys[:, 0, :] = solutions
+        if P == 1:  # the physical layout is the node layout
+            sol_phys = np.ascontiguousarray(solutions)
         else:
+            sol_phys = np.zeros((batch, P, self.rows_max), dtype=np.uint8)
             for r, pr in enumerate(partition_rows(n, P)):
                 sol_phys[:, r, :pr.num_rows] = solutions[:, pr.row_start:pr.row_stop]
         sol_phys_d = to_device(sol_phys.reshape(-1), dev, pinned=True)
-        _lib.call("s2v_shard_init", ctypes.byref(self._shard), ptr(sol_phys_d), stream_ptr())
+        _lib.call("s2v_shard_init", ctypes.byref(self._shard), ptr(cols_src), ptr(sol_phys_d),
+                  stream_ptr())
         self._host = {}
         self._ws: dict = {}
 
@@ -287,6 +294,15 @@ class PartitionedState:
         return entry[1]
 
     def invalidate(self) -> None:
+        self._host.clear()
+
+    def release(self) -> None:
+        """Drop this state's device workspaces now (embedding buffers, score
+        and backward scratch): a caller replacing states in a loop returns
+        their memory to the caching allocator at once instead of at the
+        next cycle collection.  The state stays usable (workspaces are
+        rebuilt on demand)."""
+        self._ws.clear()
         self._host.clear()
 
     def _mirror(self, name: str, tensor: torch.Tensor, shape) -> np.ndarray:
