@@ -16,8 +16,14 @@ sol = np.zeros((1, g.num_nodes), np.uint8)
 active = np.array([True])
 
 
+held = []
+
+
 def step():
+    while held:
+        held.pop().release()
     st = P.PartitionedState([g], part, solutions=sol)
+    held.append(st)
     picks, applied = solve_step(st, params, comm, sched, active)
     for v, a in zip(picks[0], applied[0]):
         if v >= 0 and a:
