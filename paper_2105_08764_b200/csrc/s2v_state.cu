@@ -471,8 +471,27 @@ int s2v_shard_init(const s2v_shard *sh, const uint32_t *cols_src, const uint8_t 
   int64_t rows = (int64_t)sh->batch * sh->num_rows;
   if (rows == 0) return S2V_OK;
   const int64_t nphys = (int64_t)sh->batch * sh->world * sh->rows_max;
-  uint32_t *bits = nullptr;
-  S2V_CUDA_CHECK(cudaMallocAsync((void **)&bits, 4 * ((nphys + 31) / 32), st));
+  // grow-only scratch per thread and device (no stream-ordered pool
+  // allocation on this path: the pool trims at synchronisations and regrows)
+  static thread_local struct {
+    int dev = -1;
+    uint32_t *p = nullptr;
+    size_t bytes = 0;
+  } scratch;
+  int dev = 0;
+  S2V_CUDA_CHECK(cudaGetDevice(&dev));
+  const size_t need = 4 * (size_t)((nphys + 31) / 32);
+  if (scratch.dev != dev || scratch.bytes < need) {
+    if (scratch.p && scratch.dev == dev) {
+      S2V_CUDA_CHECK(cudaStreamSynchronize(st));
+      cudaFree(scratch.p);
+    }
+    scratch.p = nullptr;
+    S2V_CUDA_CHECK(cudaMalloc((void **)&scratch.p, need));
+    scratch.dev = dev;
+    scratch.bytes = need;
+  }
+  uint32_t *bits = scratch.p;
   sol_bits_kernel<<<(unsigned)std::min<int64_t>(((nphys + 31) / 32 + 255) / 256, kNumSMs * 8),
                     256, 0, st>>>(sol_phys, nphys, bits);
   S2V_LAUNCH_CHECK();
@@ -480,7 +499,6 @@ int s2v_shard_init(const s2v_shard *sh, const uint32_t *cols_src, const uint8_t 
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
   shard_init_kernel<<<(unsigned)blocks, 256, 0, st>>>(*sh, cols_src, sol_phys, bits);
   S2V_LAUNCH_CHECK();
-  S2V_CUDA_CHECK(cudaFreeAsync(bits, st));
   return S2V_OK;
 }
 

@@ -175,6 +175,12 @@ class _DeviceParams:
         return self.buf.data_ptr() + self.offsets[name] * self.elem
 
 
+def _np_dtype(t: torch.dtype) -> np.dtype:
+    return {torch.float32: np.dtype(np.float32), torch.float64: np.dtype(np.float64),
+            torch.int32: np.dtype(np.int32), torch.int64: np.dtype(np.int64),
+            torch.uint8: np.dtype(np.uint8)}[t]
+
+
 def _check_dtype(state: PartitionedState, params: PolicyParams) -> None:
     if np.dtype(params.dtype) not in _DTYPE_CODES:
         raise ValueError(f"unsupported parameter dtype {params.dtype}")
@@ -786,14 +792,21 @@ def train_iterations(state: PartitionedState, actions, targets, params: PolicyPa
                   ptr(bad), it, stream_ptr())
     if tau <= 0:
         return []
-    flags = bad.to("cpu").numpy()
+    # one read-back: flags, parameters, moments and losses as one byte buffer
+    outs = (bad, dparams.buf, m_d, v_d, losses)
+    raw = torch.cat([t.reshape(-1).view(torch.uint8) for t in outs]).to("cpu").numpy()
+    parts, off = [], 0
+    for t in outs:
+        nb = t.numel() * t.element_size()
+        parts.append(raw[off:off + nb].view(_np_dtype(t.dtype)))
+        off += nb
+    flags, new_p, m_h, v_h, loss_h = parts
     done = int(np.argmax(flags != 0)) if flags.any() else tau
-    new_p = dparams.buf.to("cpu").numpy().astype(dtype)
-    for name, arr in unflatten_arrays(new_p, k).items():
+    for name, arr in unflatten_arrays(new_p.astype(dtype), k).items():
         getattr(params, name)[...] = arr
-    for name, arr in unflatten_arrays(m_d.to("cpu").numpy(), k).items():
+    for name, arr in unflatten_arrays(m_h.copy(), k).items():
         adam.m[name] = arr
-    for name, arr in unflatten_arrays(v_d.to("cpu").numpy(), k).items():
+    for name, arr in unflatten_arrays(v_h.copy(), k).items():
         adam.v[name] = arr
     adam.step += done
     dparams._flat = np.ascontiguousarray(flatten_arrays(params.as_dict()), dtype=dtype)
@@ -801,7 +814,7 @@ def train_iterations(state: PartitionedState, actions, targets, params: PolicyPa
         grads = unflatten_arrays(pack.to("cpu").numpy()[:-1].astype(dtype), k)
         name = next(nm for nm in PARAM_NAMES if not np.all(np.isfinite(grads[nm])))
         raise ValueError(f"non-finite gradient for {name}; step rejected")
-    return [float(x) / b for x in losses.to("cpu").numpy()[:tau]]
+    return [float(x) / b for x in loss_h[:tau]]
 
 
 # ---------------------------------------------------------------------------
