@@ -85,11 +85,11 @@ inline int grid_for(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kNumSMs * 16));
 }
 
-// plain cudaMalloc (setup path): stream-ordered pool allocations next to
-// torch's caching allocator measured 0.3-0.6 s per training step of stalls
+// (setup path, once per graph: the stream-ordered pool is trimmed at the
+// final synchronisation; hot paths use grow-only cudaMalloc scratch instead)
 template <class T>
-int dev_alloc(T **p, size_t count, cudaStream_t) {
-  S2V_CUDA_CHECK(cudaMalloc((void **)p, std::max<size_t>(count, 1) * sizeof(T)));
+int dev_alloc(T **p, size_t count, cudaStream_t st) {
+  S2V_CUDA_CHECK(cudaMallocAsync((void **)p, std::max<size_t>(count, 1) * sizeof(T), st));
   return S2V_OK;
 }
 
@@ -184,11 +184,10 @@ int s2v_shard_structure(int64_t n, int P, int64_t rows_max, int64_t rows,
   if (max_deg_out) *max_deg_out = h_max;
 cleanup:
 #undef S2V_TRY
-  cudaStreamSynchronize(st);
   for (void *p : {(void *)hist, (void *)entry_row, (void *)keys_out, (void *)iota,
                   (void *)iota_rows, (void *)deg_key, (void *)deg_key_out, (void *)dmax,
                   (void *)nhub, tmp})
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
   return rc;
 }
 
