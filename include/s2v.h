@@ -199,7 +199,8 @@ int s2v_active_compact(const s2v_shard *sh, int32_t *list, int64_t *n, int32_t *
                        void *stream);
 int64_t s2v_active_workspace(int64_t cap);
 
-/* Incremental-forward frontier (B = 1, P = 1; csrc/s2v_frontier.cu): the
+/* Incremental-forward frontier (B = 1, P = 1 -- P > 1: the bitmap form below;
+ * csrc/s2v_frontier.cu): the
  * rows whose round-l embedding may change after a group apply -- the picks
  * and their alive neighbours (seed, called BEFORE s2v_apply_phase2), then
  * `levels`-1 hops over the residual graph (expand, AFTER the apply).  D
@@ -213,6 +214,27 @@ int s2v_frontier_expand(const s2v_shard *sh, int levels, int32_t *D, int64_t *me
                         int64_t cap, const int32_t *act, const int64_t *act_n, int64_t act_cap,
                         void *stream);
 int64_t s2v_frontier_meta_size(int levels);
+/* P > 1 frontier on bitmaps over every rank's physical rows (B = 1;
+ * s2v_frontier_bits_words uint32 words each): seed marks this rank's picks
+ * and their alive neighbours into mbits (and clears gbits, the levels' union)
+ * BEFORE s2v_apply_phase2; the ranks all-gather mbits as [P][words]; merge
+ * ORs them, keeps newbits = the rows new at `level`, appends this rank's new
+ * rows to D / meta exactly as s2v_frontier_seed / _expand do (and, at the
+ * last level, the active-list fallback on overflow); expand marks the alive
+ * neighbours of this rank's newbits rows for the next level (AFTER the
+ * apply).  nodes: the global node ids in gbits (the global sum's dirty rows;
+ * n[0] = count, n[1] = 0). */
+int64_t s2v_frontier_bits_words(const s2v_shard *sh);
+int s2v_frontier_bits_seed(const s2v_shard *sh, const int64_t *picks, int d, int levels,
+                           int64_t *meta, uint32_t *mbits, uint32_t *gbits, void *stream);
+int s2v_frontier_bits_expand(const s2v_shard *sh, const uint32_t *newbits, uint32_t *mbits,
+                             void *stream);
+int s2v_frontier_bits_merge(const s2v_shard *sh, const uint32_t *gathered, uint32_t *gbits,
+                            uint32_t *newbits, int level, int levels, int32_t *D, int64_t *meta,
+                            int32_t *mark, int64_t cap, const int32_t *act, const int64_t *act_n,
+                            int64_t act_cap, void *stream);
+int s2v_frontier_bits_nodes(const s2v_shard *sh, const uint32_t *gbits, int32_t *nodes,
+                            int64_t *n, void *stream);
 
 /* g[b][k] = numpy pairwise sum over the N nodes of slot b of h[.,k]; h must
  * hold every rank's rows (after an all-gather when P>1).  Replaces
@@ -234,8 +256,9 @@ int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
                         size_t workspace_bytes, uint8_t *last, int full,
                         const int32_t *dirty_rows, const int64_t *ndirty,
                         const int32_t *trow_phys, void *stream);
-/* (dirty_rows, ndirty: incremental forward, P = 1 -- only the leaves holding
- * one of these rows (every row whose embedding changed) are recomputed.
+/* (dirty_rows, ndirty: incremental forward -- the global node ids whose
+ * embedding changed (P = 1: the frontier rows; P > 1: s2v_frontier_bits_nodes);
+ * only the leaves holding one of them are recomputed.
  * trow_phys: P > 1 (NULL at P = 1) -- every rank's e12 table row by physical
  * row (s2v_trow + the all-gather of round 2), which classifies every node of
  * the gathered buffer: 0 dead, max_deg + 1 in S, else alive.)  Workspace
@@ -254,7 +277,7 @@ int s2v_score(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, const voi
               const void *theta6, const void *theta7, const uint8_t *cand_override,
               int mode, void *scores, uint64_t *block_keys, int64_t *counts, void *stream);
 int s2v_score_blocks(const s2v_shard *sh);
-/* Scores of an active-row list (B = 1, P = 1, K = 64 fp32) with a per-row
+/* Scores of an active-row list (B = 1, K = 64 fp32) with a per-row
  * cache of the theta7 terms fl(relu(u2_k) theta7_{K+k}), prod_cache[rows][64]:
  * rows == NULL scores every list row and fills the cache; otherwise the
  * cache is refreshed for rows[0, nrows[0]) (the incremental frontier) and

@@ -1491,8 +1491,6 @@ int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
                         const int32_t *trow_phys, void *stream) {
   if (sh->world != 1 && !trow_phys)
     return fail(S2V_EINVAL, "residual colsum at P > 1 needs every rank's e12 rows (trow)");
-  if (sh->world != 1 && dirty_rows)
-    return fail(S2V_EINVAL, "dirty-row colsum needs P = 1");
   if (max_deg < 0 || !h1_table) return fail(S2V_EINVAL, "bad residual colsum args");
   cudaStream_t st = as_stream(stream);
   const size_t elem = dt == S2V_F32 ? 4 : 8;
@@ -1561,8 +1559,8 @@ int s2v_score_cached(const s2v_shard *sh, const float *h, const float *u1, const
                      const float *theta7, int mode, float *prod_cache, const int32_t *rows,
                      const int64_t *nrows, float *scores, uint64_t *block_keys, int64_t *counts,
                      void *stream) {
-  if (!sh->active || sh->batch != 1 || sh->world != 1 || !prod_cache)
-    return fail(S2V_EINVAL, "cached scores need an active-row list, B = 1, P = 1");
+  if (!sh->active || sh->batch != 1 || !prod_cache)
+    return fail(S2V_EINVAL, "cached scores need an active-row list, B = 1");
   cudaStream_t st = as_stream(stream);
   S2V_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(int64_t), st));
   const int nblk = s2v_score_blocks(sh);

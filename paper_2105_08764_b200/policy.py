@@ -376,7 +376,8 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
         dc = comm.device_comm() if state.world > 1 else None
         if dc is not None and dc.supports_push and k == 64 and dt == _lib.S2V_F32:
             # fused halo exchange: the kernel stores each row into every peer
-            peers = _peer_list(state, dc, f"h{layer if tape else layer % 2}/{len(hs)}", h_out,
+            peers = _peer_list(state, dc,
+                               f"h{layer if (tape or persist) else layer % 2}/{len(hs)}", h_out,
                                True)
             _lib.call("s2v_embed_round_peers", dt, state.shard_ref(), dparams.ptr("theta4"),
                       ptr(table), k, max_deg, ptr(h_prev), ptr(h_out), ptr(peers), state.world,
@@ -387,7 +388,7 @@ def _forward_rounds(state: PartitionedState, dparams: _DeviceParams, num_layers:
             _lib.call("s2v_embed_round", dt, state.shard_ref(), dparams.ptr("theta4"),
                       ptr(table), k, max_deg, ptr(h_prev), ptr(h_out), ptr(m_out), st)
             _allgather_rows(state, comm, h_out, k, "embed_fwd",
-                            name=f"h{layer if tape else layer % 2}/{len(hs)}")
+                            name=f"h{layer if (tape or persist) else layer % 2}/{len(hs)}")
         sh.active, sh.active_n, sh.active_ptr, sh.active_cols = outer
         if timer is not None:
             ev1.record()

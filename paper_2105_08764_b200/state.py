@@ -95,9 +95,10 @@ class _ShardStructure:
         # column ids, the column lookup (stable argsort by neighbour id) and
         # the descending-degree processing order (rows above the hub degree
         # go to the CTA-cooperative kernel)
-        self.row_ptr = to_device(row_ptr_g[part.row_start:part.row_stop + 1] - lo, device,
-                                 pinned=True)
-        nbr = to_device(cols_g[lo:hi], device, pinned=True) if self.nnz else \
+        # (one-shot uploads: pageable copies -- page-locking 256 MB first costs
+        # more than it saves)
+        self.row_ptr = to_device(row_ptr_g[part.row_start:part.row_stop + 1] - lo, device)
+        nbr = to_device(cols_g[lo:hi], device) if self.nnz else \
             torch.zeros(1, dtype=torch.int32, device=device)
         self.cols0 = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=device)
         self.col_ptr = torch.empty(n + 1, dtype=torch.int64, device=device)

@@ -225,3 +225,42 @@ def test_d1_schedule_is_stepwise_argmax_at_p_ranks(p):
         assert pk == picks[0]
         assert r.cover == sorted(pk)
         assert r.policy_evals == len(pk)
+
+
+@pytest.mark.parametrize("p,inc_cap", [(2, 0.25), (3, 0.25), (2, 0.0)])
+def test_incremental_episode_at_p_ranks(p, inc_cap, monkeypatch):
+    """The incremental forward at P > 1 (frontier levels built from
+    all-gathered bitmaps, every rank recomputing only its frontier rows, the
+    global sum refreshing only leaves of changed nodes), switched on from
+    the first compaction: the whole episode's trace equals the P = 1 loop
+    over every row; inc_cap = 0 makes every local frontier overflow."""
+    from paper_2105_08764_b200.inference import DeviceEpisode
+    monkeypatch.setattr(DeviceEpisode, "COMPACT_MIN_ROWS", 0)
+    g = P.generate_rmat(13, 16, 4)
+    params = P.PolicyParams.initialize(64, 5, seed=8)
+    sched = P.SelectionSchedule.adaptive()
+
+    def run(world, compact):
+        def worker(comm):
+            st = P.PartitionedState([g], P.partition_rows(g.num_nodes, comm.size)[comm.rank])
+            ep = DeviceEpisode(st, params, comm, sched, 4, use_graph=False, compact=compact)
+            trace = []
+            while True:
+                tp, ta, te, active = ep.run_chunk()
+                trace.append((tp.copy(), ta.copy(), te.copy()))
+                if not active.any():
+                    break
+            return trace, (ep._mode[2] if compact else None)
+        return P.run_workers(world, worker)
+
+    (t_f, _), = run(1, False)
+    monkeypatch.setattr(DeviceEpisode, "INC_RATIO", 1e9)
+    monkeypatch.setattr(DeviceEpisode, "LIST_FRAC", 1.0)
+    monkeypatch.setattr(DeviceEpisode, "INC_CAP", inc_cap)
+    if inc_cap == 0.0:
+        monkeypatch.setattr(DeviceEpisode, "INC_MIN", 0)
+    for trace, inc_used in run(p, True):
+        assert inc_used
+        assert len(trace) == len(t_f)
+        for i, ((a, b, c), (x, y, z)) in enumerate(zip(trace, t_f)):
+            assert np.array_equal(a, x) and np.array_equal(b, y) and np.array_equal(c, z), i
