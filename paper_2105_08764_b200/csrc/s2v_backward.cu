@@ -1257,9 +1257,9 @@ __global__ void __launch_bounds__(256, 4) gather64_tiles_kernel(s2v_shard sh,
       if (r < 0) continue;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       if (s_e1[lr] > s_e0[lr])
-        acc = gather_row64(s_e0[lr], s_e1[lr], sh.cols, src, sub, hmask, hbase, hot_rows,
-                           pol_hot, pol_cold, nullptr, nullptr,
-                           (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
+        acc = gather_row64<false, true>(
+            s_e0[lr], s_e1[lr], sh.cols, src, sub, hmask, hbase, hot_rows, pol_hot, pol_cold,
+            nullptr, nullptr, (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
       st4(out + r * 64 + 4 * sub, acc);
     }
     cur ^= 1;

@@ -72,7 +72,10 @@ __device__ __forceinline__ uint32_t source_row(uint32_t c, const int32_t *__rest
 
 // Sequential alive-neighbour sum of one row by one half-warp (lanes `sub`
 // 0..15 of mask `hmask`), float4 per lane.
-template <bool TABLE = false>
+// PF: prefetch the second half of each 16-neighbour group into L2 while the
+// first half's rows are in flight (spmm_t: 4.22 -> 3.84 ms per B = 2 launch;
+// the forward round, at its 64-register budget, does not gain from it)
+template <bool TABLE = false, bool PF = false>
 __device__ __forceinline__ float4 gather_row64(int64_t e, const int64_t e1,
                                                const uint32_t *__restrict__ cols,
                                                const float *__restrict__ h_in, int sub,
@@ -103,6 +106,14 @@ __device__ __forceinline__ float4 gather_row64(int64_t e, const int64_t e1,
           const float *src = h_in + (int64_t)c[q] * 64 + sub * 4;
           v[q] = ldg_f4_pol(src, c[q] - hot_lo < hot_rows ? pol_hot : pol_cold);
         }
+      }
+      if (PF && half == 0 && cnt > 8) {
+        // the second half's rows into L2 while these 8 are in flight (no
+        // registers held): lane l prefetches the line of row 8 + (l & 7)
+        // holding its half of the 256-byte row
+        const uint32_t cn = __shfl_sync(hmask, mine, hbase + 8 + (sub & 7));
+        if (!(cn & S2V_DEAD) && !TABLE)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(h_in + (int64_t)cn * 64 + (sub >> 3) * 32));
       }
 #pragma unroll
       for (int q = 0; q < 8; q++)
