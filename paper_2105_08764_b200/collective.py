@@ -109,6 +109,7 @@ class _DeviceComm:
         _lib.call("s2v_comm_init", buf, world, rank, ctypes.byref(handle))
         self.handle = handle
         self.world, self.rank = world, rank
+        self._scratch: dict = {}  # all-gather scratch of the ordered all-reduce, by bytes
 
     supports_push = False
 
@@ -125,9 +126,8 @@ class _DeviceComm:
         if count == 0:
             return
         nbytes = count * (4 if kind == 2 else 8)
-        buf = self._scratch.get(nbytes) if hasattr(self, "_scratch") else None
+        buf = self._scratch.get(nbytes)
         if buf is None:
-            self._scratch = getattr(self, "_scratch", {})
             buf = self._scratch[nbytes] = torch.empty(self.world * nbytes, dtype=torch.uint8,
                                                       device="cuda")
         self._lib.call("s2v_comm_allreduce_ordered", self.handle, buf_ptr, count, kind,
@@ -146,9 +146,9 @@ class _PeerTransport:
     registration, cached per workspace by the callers); the forward round
     kernel pushes each output row into every peer's halo buffer itself
     (s2v_embed_round_peers -- the exchange is fused into the compute), and
-    ranks order producer/consumer with per-peer flags written and waited on
-    by the CUDA streams (no host barrier, no host synchronisation, no SM
-    spinning).  All-reduces push each rank's vector into every peer's
+    ranks order producer/consumer on the CUDA streams: per-peer flags written
+    and waited on by the streams for process ranks, CUDA events for thread
+    ranks (no host synchronisation of GPU work, no SM spinning).  All-reduces push each rank's vector into every peer's
     scratch row [rank] and sum the P rows in ascending rank order on the
     device (s2v_sum_ranks_typed): the reference's order
     (collective.py:100-117), identical bits on every rank.
