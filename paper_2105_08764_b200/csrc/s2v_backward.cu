@@ -1208,7 +1208,8 @@ __global__ void __launch_bounds__(256, 4) gather64_tiles_kernel(s2v_shard sh,
                                                                 const float *__restrict__ src,
                                                                 float *__restrict__ out,
                                                                 uint32_t hot_rows,
-                                                                int *__restrict__ tile_counter) {
+                                                                int *__restrict__ tile_counter,
+                                                                int sparse_max) {
   __shared__ int32_t s_raw[2][kGTile];
   __shared__ int64_t s_e0[kGTile], s_e1[kGTile];
   __shared__ int32_t s_rows[kGTile];
@@ -1248,19 +1249,35 @@ __global__ void __launch_bounds__(256, 4) gather64_tiles_kernel(s2v_shard sh,
       s_e0[tid] = e0;
       s_e1[tid] = e1;
     }
-    __syncthreads();
+    // tiles whose rows all have <= sparse_max entries: one 8-lane group per
+    // row, every row of the tile in flight at once (as round64_kernel)
+    const bool sparse =
+        __syncthreads_and(tid >= kGTile || s_e1[tid] - s_e0[tid] <= sparse_max);
     if (tid < kGTile) prefetch_rows(s_tiles[cur ^ 1], cur ^ 1);
-#pragma unroll
-    for (int q = 0; q < 2; q++) {
-      const int lr = hw + 16 * q;
+    if (sparse) {
+      const int lr = tid >> 3, l8 = tid & 7;
       const int64_t r = s_rows[lr];
-      if (r < 0) continue;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (s_e1[lr] > s_e0[lr])
-        acc = gather_row64<false, true>(
-            s_e0[lr], s_e1[lr], sh.cols, src, sub, hmask, hbase, hot_rows, pol_hot, pol_cold,
-            nullptr, nullptr, (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
-      st4(out + r * 64 + 4 * sub, acc);
+      if (r >= 0) {
+        float4 a0, a1;
+        gather_row64_g8(s_e0[lr], s_e1[lr], sh.cols, src, l8, 0xFFu << (tid & 24), tid & 24,
+                        hot_rows, pol_hot, pol_cold, nullptr, nullptr,
+                        (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max), a0, a1);
+        st4(out + r * 64 + 4 * l8, a0);
+        st4(out + r * 64 + 32 + 4 * l8, a1);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const int lr = hw + 16 * q;
+        const int64_t r = s_rows[lr];
+        if (r < 0) continue;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (s_e1[lr] > s_e0[lr])
+          acc = gather_row64<false, true>(
+              s_e0[lr], s_e1[lr], sh.cols, src, sub, hmask, hbase, hot_rows, pol_hot, pol_cold,
+              nullptr, nullptr, (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
+        st4(out + r * 64 + 4 * sub, acc);
+      }
     }
     cur ^= 1;
   }
@@ -1429,8 +1446,13 @@ int s2v_gather(s2v_dtype dt, const s2v_shard *sh, int K, const void *src, void *
       }
       S2V_CUDA_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), st));
       const int64_t ntiles = (rows + kGTile - 1) / kGTile;
+      static const int sparse_max = [] {
+        const char *e = getenv("S2V_SPARSE_MAX");
+        return e ? atoi(e) : S2V_HUB_DEGREE;
+      }();
       gather64_tiles_kernel<<<(int)std::min<int64_t>(std::max<int64_t>(ntiles, 1), kNumSMs * 4),
-                              256, 0, st>>>(*sh, (const float *)src, (float *)out, hot, counter);
+                              256, 0, st>>>(*sh, (const float *)src, (float *)out, hot, counter,
+                                            sparse_max);
     } else {
       gather64_kernel<<<kNumSMs * 8, 256, 0, st>>>(*sh, (const float *)src, (float *)out, hot);
     }

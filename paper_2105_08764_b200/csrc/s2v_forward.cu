@@ -132,6 +132,14 @@ __global__ void __launch_bounds__(256) round_generic_kernel(
 //           adds give the same sums; the 2.4 MB table stays in L1/L2, so the
 //           round reads the CSR and rdeg instead of 16 GB of neighbour rows.
 constexpr int kTileRows = 32;
+// tiles whose rows all have at most this many entries gather one row per
+// 8-lane group (all 32 rows of the tile in flight at once) instead of one row
+// per half-warp, two rows at a time.  Measured on cfg3 (round ms): 0 (off)
+// 2.43, 16: 2.41, 32: 2.28, 64: 2.24, 128: 2.237, 512: 2.234, 4096: 2.232 —
+// more rows in flight beats the longer per-row chains at every degree below
+// the hub cut, so the default is the hub degree (every non-hub tile).
+// S2V_SPARSE_MAX overrides it (0 turns the mode off) for A/B runs.
+constexpr int kSparseMax = S2V_HUB_DEGREE;
 
 // h1_table[t][k] = the round-1 output of a row whose e12 row is t: the
 // round kernel's epilogue with m = 0 (FMA chain over zeros, + e12, relu).
@@ -157,7 +165,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
     s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ table, int max_deg,
     const float *__restrict__ h_in, float *__restrict__ h_out, float *__restrict__ m_out,
     int *__restrict__ tile_counter, uint32_t hot_rows, float *const *__restrict__ peers,
-    int npeers, const int32_t *__restrict__ deg_src) {
+    int npeers, const int32_t *__restrict__ deg_src, int sparse_max) {
   // deg_src (TABLE): residual degree by physical row -- every rank's rows
   // at P > 1 (s2v_trow + exchange), this shard's rdeg at P = 1
   __shared__ __align__(16) float thT[64][64 + 4];        // thT[p][k] = theta4[k][p]
@@ -223,7 +231,31 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       s_e1[tid] = e1;
       s_trow[tid] = trow;
     }
-    __syncthreads();
+    // sparse tile (every row <= kSparseMax entries, the bulk of a late
+    // episode and of R-MAT): one 8-lane group per row, all 32 rows of the
+    // tile at once instead of two rows in turn per half-warp
+    const bool sparse =
+        __syncthreads_and(tid >= kTileRows || s_e1[tid] - s_e0[tid] <= sparse_max);
+    if (sparse) {
+      const int lr = tid >> 3, l8 = tid & 7;
+      const unsigned qmask = 0xFFu << (tid & 24);
+      const int qbase = tid & 24;
+      const int64_t r = s_rows[lr];
+      const int64_t e0 = s_e0[lr], e1 = s_e1[lr];
+      const uint32_t *cl = sh.active_ptr ? sh.active_cols : sh.cols;
+      const uint8_t *sol_of = sh.active_ptr ? sh.sol : nullptr;
+      const uint32_t hot_lo =
+          TABLE ? 0u : (uint32_t)(r >= 0 ? (r / sh.num_rows) * sh.world * sh.rows_max : 0);
+      float4 a0, a1;
+      gather_row64_g8<TABLE>(e0, e1, cl, h_in, l8, qmask, qbase, hot_rows, pol_hot, pol_cold,
+                             deg_src, sol_of, hot_lo, a0, a1);
+      *reinterpret_cast<float4 *>(&ms[lr][4 * l8]) = a0;
+      *reinterpret_cast<float4 *>(&ms[lr][32 + 4 * l8]) = a1;
+      if (m_out && r >= 0) {
+        *reinterpret_cast<float4 *>(m_out + r * 64 + 4 * l8) = a0;
+        *reinterpret_cast<float4 *>(m_out + r * 64 + 32 + 4 * l8) = a1;
+      }
+    } else {
     // ---- gather: each half-warp handles rows hw and hw+16 of the tile
 #pragma unroll
     for (int q = 0; q < 2; q++) {
@@ -237,6 +269,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
             TABLE ? 0u : (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
       *reinterpret_cast<float4 *>(&ms[lr][sub * 4]) = acc;
       if (m_out && r >= 0) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
+    }
     }
     __syncthreads();
     if (tid < kTileRows) prefetch_rows(s_tiles[cur ^ 1], cur ^ 1);
@@ -1283,9 +1316,13 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
           (float *)h_out, (float *)m_out, hub_counter, hot_rows, peers, npeers, deg_src);
     }, &ss);
     if (rc) return rc;
+    static const int sparse_max = [] {
+      const char *e = getenv("S2V_SPARSE_MAX");
+      return e ? atoi(e) : kSparseMax;
+    }();
     kern<<<grid, 256, 0, st>>>(*sh, (const float *)theta4, (const float *)table, max_deg,
                                (const float *)h_in, (float *)h_out, (float *)m_out, counter,
-                               hot_rows, peers, npeers, deg_src);
+                               hot_rows, peers, npeers, deg_src, sparse_max);
     S2V_LAUNCH_CHECK();
     if (ss) S2V_CUDA_CHECK(cudaStreamWaitEvent(st, ss->done, 0));
     S2V_LAUNCH_CHECK();

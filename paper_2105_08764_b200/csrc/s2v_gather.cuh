@@ -124,6 +124,55 @@ __device__ __forceinline__ float4 gather_row64(int64_t e, const int64_t e1,
 }
 
 
+// Sequential alive-neighbour sum of one row by an 8-lane group (lanes l8 =
+// 0..7 of mask qmask / base qbase): lane l8 holds the float4s l8 and l8 + 8
+// of the 64-float row (a0, a1); neighbour ids 8 at a time (one per lane),
+// rows 4 at a time (8 float4 per lane in flight), added in ascending order --
+// the same sums, bit for bit, as gather_row64.  Four rows per warp instead of
+// one: a tile's 32 rows are all in flight at once.
+template <bool TABLE = false>
+__device__ __forceinline__ void gather_row64_g8(const int64_t e0, const int64_t e1,
+                                                const uint32_t *__restrict__ cols,
+                                                const float *__restrict__ h_in, int l8,
+                                                unsigned qmask, int qbase, uint32_t hot_rows,
+                                                uint64_t pol_hot, uint64_t pol_cold,
+                                                const int32_t *__restrict__ deg_of,
+                                                const uint8_t *__restrict__ sol_of,
+                                                uint32_t hot_lo, float4 &a0, float4 &a1) {
+  a0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  a1 = a0;
+  const int cnt = (int)(e1 - e0);
+  for (int e8 = 0; e8 < cnt; e8 += 8) {
+    const uint32_t id = source_row<TABLE>(
+        e8 + l8 < cnt ? ldg_u32_pol(cols + e0 + e8 + l8, pol_cold) : S2V_DEAD, deg_of, sol_of);
+#pragma unroll
+    for (int g = 0; g < 2; g++) {  // neighbours e8 + 4g .. + 3
+      if (e8 + 4 * g >= cnt) break;
+      uint32_t c[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) c[q] = __shfl_sync(qmask, id, qbase + 4 * g + q);
+      float4 v0[4], v1[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        if (c[q] & S2V_DEAD) {
+          v0[q] = v1[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          const float *src = h_in + (int64_t)c[q] * 64;
+          const uint64_t pol = c[q] - hot_lo < hot_rows ? pol_hot : pol_cold;
+          v0[q] = ldg_f4_pol(src + 4 * l8, pol);
+          v1[q] = ldg_f4_pol(src + 32 + 4 * l8, pol);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+        if (!(c[q] & S2V_DEAD)) {
+          add4(a0, v0[q]);
+          add4(a1, v1[q]);
+        }
+    }
+  }
+}
+
 // CTA-cooperative sequential gather of one hub row (degree > S2V_HUB_DEGREE):
 // half-warps 1..15 stage 8 neighbour rows each (kHubBatch = 120 per batch)
 // into a double-buffered shared ring while half-warp 0 adds the previous
