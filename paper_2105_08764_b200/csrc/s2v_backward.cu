@@ -1209,7 +1209,7 @@ __global__ void __launch_bounds__(256, 4) gather64_tiles_kernel(s2v_shard sh,
                                                                 float *__restrict__ out,
                                                                 uint32_t hot_rows,
                                                                 int *__restrict__ tile_counter,
-                                                                int sparse_max) {
+                                                                int sparse_max, int pf) {
   __shared__ int32_t s_raw[2][kGTile];
   __shared__ int64_t s_e0[kGTile], s_e1[kGTile];
   __shared__ int32_t s_rows[kGTile];
@@ -1261,7 +1261,7 @@ __global__ void __launch_bounds__(256, 4) gather64_tiles_kernel(s2v_shard sh,
         float4 a0, a1;
         gather_row64_g8(s_e0[lr], s_e1[lr], sh.cols, src, l8, 0xFFu << (tid & 24), tid & 24,
                         hot_rows, pol_hot, pol_cold, nullptr, nullptr,
-                        (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max), a0, a1);
+                        (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max), a0, a1, pf);
         st4(out + r * 64 + 4 * l8, a0);
         st4(out + r * 64 + 32 + 4 * l8, a1);
       }
@@ -1452,7 +1452,7 @@ int s2v_gather(s2v_dtype dt, const s2v_shard *sh, int K, const void *src, void *
       }();
       gather64_tiles_kernel<<<(int)std::min<int64_t>(std::max<int64_t>(ntiles, 1), kNumSMs * 4),
                               256, 0, st>>>(*sh, (const float *)src, (float *)out, hot, counter,
-                                            sparse_max);
+                                            sparse_max, g8_prefetch());
     } else {
       gather64_kernel<<<kNumSMs * 8, 256, 0, st>>>(*sh, (const float *)src, (float *)out, hot);
     }

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
     s2v_shard sh, const float *__restrict__ theta4, const float *__restrict__ table, int max_deg,
     const float *__restrict__ h_in, float *__restrict__ h_out, float *__restrict__ m_out,
     int *__restrict__ tile_counter, uint32_t hot_rows, float *const *__restrict__ peers,
-    int npeers, const int32_t *__restrict__ deg_src, int sparse_max) {
+    int npeers, const int32_t *__restrict__ deg_src, int sparse_max, int pf) {
   // deg_src (TABLE): residual degree by physical row -- every rank's rows
   // at P > 1 (s2v_trow + exchange), this shard's rdeg at P = 1
   __shared__ __align__(16) float thT[64][64 + 4];        // thT[p][k] = theta4[k][p]
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
           TABLE ? 0u : (uint32_t)(r >= 0 ? (r / sh.num_rows) * sh.world * sh.rows_max : 0);
       float4 a0, a1;
       gather_row64_g8<TABLE>(e0, e1, cl, h_in, l8, qmask, qbase, hot_rows, pol_hot, pol_cold,
-                             deg_src, sol_of, hot_lo, a0, a1);
+                             deg_src, sol_of, hot_lo, a0, a1, !TABLE && pf);
       *reinterpret_cast<float4 *>(&ms[lr][4 * l8]) = a0;
       *reinterpret_cast<float4 *>(&ms[lr][32 + 4 * l8]) = a1;
       if (m_out && r >= 0) {
@@ -1322,7 +1322,7 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
     }();
     kern<<<grid, 256, 0, st>>>(*sh, (const float *)theta4, (const float *)table, max_deg,
                                (const float *)h_in, (float *)h_out, (float *)m_out, counter,
-                               hot_rows, peers, npeers, deg_src, sparse_max);
+                               hot_rows, peers, npeers, deg_src, sparse_max, g8_prefetch());
     S2V_LAUNCH_CHECK();
     if (ss) S2V_CUDA_CHECK(cudaStreamWaitEvent(st, ss->done, 0));
     S2V_LAUNCH_CHECK();

@@ -138,13 +138,19 @@ __device__ __forceinline__ void gather_row64_g8(const int64_t e0, const int64_t 
                                                 uint64_t pol_hot, uint64_t pol_cold,
                                                 const int32_t *__restrict__ deg_of,
                                                 const uint8_t *__restrict__ sol_of,
-                                                uint32_t hot_lo, float4 &a0, float4 &a1) {
+                                                uint32_t hot_lo, float4 &a0, float4 &a1,
+                                                bool pf = false) {
   a0 = make_float4(0.f, 0.f, 0.f, 0.f);
   a1 = a0;
   const int cnt = (int)(e1 - e0);
   for (int e8 = 0; e8 < cnt; e8 += 8) {
     const uint32_t id = source_row<TABLE>(
         e8 + l8 < cnt ? ldg_u32_pol(cols + e0 + e8 + l8, pol_cold) : S2V_DEAD, deg_of, sol_of);
+    if (pf && l8 >= 4 && !(id & S2V_DEAD)) {  // rows 4..7 toward L2 while 0..3 load
+      const float *src = h_in + (int64_t)id * 64;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 32));
+    }
 #pragma unroll
     for (int g = 0; g < 2; g++) {  // neighbours e8 + 4g .. + 3
       if (e8 + 4 * g >= cnt) break;
@@ -171,6 +177,17 @@ __device__ __forceinline__ void gather_row64_g8(const int64_t e0, const int64_t 
         }
     }
   }
+}
+
+// gather_row64_g8 prefetches rows 4..7 of each 8-id group into L2 while rows
+// 0..3 load (measured: round 2.306 -> 2.288 ms at cfg3, spmm_t 3.84 -> 3.76
+// ms per B = 2 launch); S2V_G8_PF=0 turns it off for A/B runs
+inline int g8_prefetch() {
+  static const int v = [] {
+    const char *e = getenv("S2V_G8_PF");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
 }
 
 // CTA-cooperative sequential gather of one hub row (degree > S2V_HUB_DEGREE):
