@@ -264,3 +264,40 @@ def test_incremental_episode_at_p_ranks(p, inc_cap, monkeypatch):
         assert len(trace) == len(t_f)
         for i, ((a, b, c), (x, y, z)) in enumerate(zip(trace, t_f)):
             assert np.array_equal(a, x) and np.array_equal(b, y) and np.array_equal(c, z), i
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_device_solve_step_at_p_ranks(p, monkeypatch):
+    """solve_step at P > 1 merges every rank's top-d keys and sums the apply
+    info on the device (_solve_step_device): picks, applied flags, the
+    solution bits and the residual counts equal the P = 1 device path and
+    the host-merge path at P ranks, step for step (adaptive d, B = 32 --
+    a device-u1 shape -- with inactive slots)."""
+    from paper_2105_08764_b200 import inference as inf
+    graphs = [P.generate_ba(500, 4, 40 + i) for i in range(32)]
+    params = P.PolicyParams.initialize(32, 3, seed=2)
+    sched = P.SelectionSchedule.adaptive()
+    active = np.ones(32, bool)
+    active[[1, 30]] = False
+
+    def run(world, device):
+        def worker(comm):
+            if not device:
+                monkeypatch.setattr(inf, "_device_loop_ok", lambda *a: False)
+            else:
+                assert inf._device_loop_ok(P.PartitionedState(
+                    graphs, P.partition_rows(500, comm.size)[comm.rank]), params, comm, sched)
+            st = P.PartitionedState(graphs, P.partition_rows(500, comm.size)[comm.rank])
+            out = [inf.solve_step(st, params, comm, sched, active) for _ in range(4)]
+            sol = comm.all_gather(st.sol.copy(), axis=-1)
+            return out, sol, st.residual_counts(comm)
+        try:
+            return P.run_workers(world, worker)
+        finally:
+            monkeypatch.undo()
+    ref_out, ref_sol, ref_res = run(1, True)[0]
+    for device in (True, False):
+        for out, sol, res in run(p, device):
+            for (pd, ad), (pr, ar) in zip(out, ref_out):
+                assert np.array_equal(pd, pr) and np.array_equal(ad, ar)
+            assert np.array_equal(sol, ref_sol) and np.array_equal(res, ref_res)
