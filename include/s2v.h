@@ -73,7 +73,8 @@ typedef struct {
                               rest, each by descending degree; NULL = identity */
   int64_t n_hub;           /* rows handled by the CTA-cooperative hub kernel */
   const int32_t *active;   /* NULL, or the active-row list (B = 1; local rows,
-                              any P; the compact CSR below only at P = 1): a
+                              any P; the compact CSR below at P > 1 needs
+                              active_sol): a
                               stable subsequence of `order` holding every row
                               with rdeg > 0 (s2v_active_compact); the
                               forward rounds and the scorer then visit only
@@ -87,6 +88,11 @@ typedef struct {
                                  when it was built; one that died since has
                                  an endpoint in S, so rounds test sol[nbr] */
   const uint32_t *active_cols;
+  const uint8_t *active_sol;  /* P > 1 with active_ptr: S of every physical
+                                 row ([B*P*rows_max], this rank's and its
+                                 peers', kept current by s2v_sol_mark) for
+                                 the compact CSR's neighbour test; NULL at
+                                 P = 1 (the test reads sol) */
 } s2v_shard;
 
 #define S2V_HUB_DEGREE 4096
@@ -193,11 +199,18 @@ int s2v_trow(const s2v_shard *sh, int max_deg, int32_t *trow_phys, void *stream)
  * active_cols.  `cap` bounds n[0] (host-side capacity of
  * list, tmp); ws holds s2v_active_workspace(cap) int64.  The rows dropped
  * never come back: a residual degree only decreases during an episode
- * (state.py:173-208).  B = 1; the compact CSR outputs only at P = 1. */
+ * (state.py:173-208).  B = 1, any P (at P > 1 rounds reading the compact
+ * CSR need s2v_shard.active_sol). */
 int s2v_active_compact(const s2v_shard *sh, int32_t *list, int64_t *n, int32_t *tmp,
                        int64_t *ws, int64_t cap, int64_t *row_ptr_out, uint32_t *cols_out,
                        void *stream);
 int64_t s2v_active_workspace(int64_t cap);
+/* sol_all[phys(b, picks[b*d+j])] = 1 for every applied pick (picks global
+ * node ids, -1 padded, identical on every rank after the key merge): keeps
+ * the all-rank S of s2v_shard.active_sol current after a group apply
+ * (inference.py:125-146 applies the same picks on every rank). */
+int s2v_sol_mark(const s2v_shard *sh, const int64_t *picks, const uint8_t *applied, int d,
+                 uint8_t *sol_all, void *stream);
 
 /* Incremental-forward frontier (B = 1, P = 1 -- P > 1: the bitmap form below;
  * csrc/s2v_frontier.cu): the

@@ -59,6 +59,7 @@ class s2v_shard(ctypes.Structure):
         ("active_n", ctypes.c_void_p),
         ("active_ptr", ctypes.c_void_p),
         ("active_cols", ctypes.c_void_p),
+        ("active_sol", ctypes.c_void_p),
     ]
 
 
@@ -97,6 +98,7 @@ _SIGNATURES = {
     "s2v_frontier_bits_merge": ([_SH, _P, _P, _P, _I, _I, _P, _P, _P, _I64, _P, _P, _I64, _P], _I),
     "s2v_frontier_bits_nodes": ([_SH, _P, _P, _P, _P], _I),
     "s2v_active_compact": ([_SH, _P, _P, _P, _P, _I64, _P, _P, _P], _I),
+    "s2v_sol_mark": ([_SH, _P, _P, _I, _P, _P], _I),
     "s2v_active_workspace": ([_I64], _I64),
     "s2v_score": ([_I, _SH, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P], _I),
     "s2v_score_blocks": ([_SH], _I),
@@ -219,7 +221,7 @@ KERNELS_PER_CALL = {
     "s2v_reduce_partials": 1, "s2v_head_backward": 1, "s2v_adam": 1, "s2v_theta2_einsum": 2,
     "s2v_u1": 1, "s2v_select": 1, "s2v_trace": 1,
     "s2v_h1_table": 1, "s2v_embed_round2_table": 1, "s2v_trow": 1, "s2v_colsum_residual": 3,
-    "s2v_active_compact": 3, "s2v_score_cached": 2, "s2v_frontier_seed": 3,
+    "s2v_active_compact": 3, "s2v_sol_mark": 1, "s2v_score_cached": 2, "s2v_frontier_seed": 3,
     "s2v_frontier_expand": 9, "s2v_frontier_bits_seed": 3, "s2v_frontier_bits_expand": 2,
     "s2v_frontier_bits_merge": 4, "s2v_frontier_bits_nodes": 1, "s2v_adam_pack": 2, "s2v_segment_copy": 1,
     "s2v_merge_rank_keys": 1, "s2v_sum_ranks": 1, "s2v_sub_i64": 1, "s2v_sum_ranks_typed": 1,

@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       const int64_t r = s_rows[lr];
       const int64_t e0 = s_e0[lr], e1 = s_e1[lr];
       const uint32_t *cl = sh.active_ptr ? sh.active_cols : sh.cols;
-      const uint8_t *sol_of = sh.active_ptr ? sh.sol : nullptr;
+      const uint8_t *sol_of = sh.active_ptr ? (sh.active_sol ? sh.active_sol : sh.sol) : nullptr;
       const uint32_t hot_lo =
           TABLE ? 0u : (uint32_t)(r >= 0 ? (r / sh.num_rows) * sh.world * sh.rows_max : 0);
       float4 a0, a1;
@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
       if (s_e1[lr] > s_e0[lr])
         acc = gather_row64<TABLE>(
             s_e0[lr], s_e1[lr], sh.active_ptr ? sh.active_cols : sh.cols, h_in, sub, hmask, hbase,
-            hot_rows, pol_hot, pol_cold, deg_src, sh.active_ptr ? sh.sol : nullptr,
+            hot_rows, pol_hot, pol_cold, deg_src,
+            sh.active_ptr ? (sh.active_sol ? sh.active_sol : sh.sol) : nullptr,
             TABLE ? 0u : (uint32_t)((r / sh.num_rows) * sh.world * sh.rows_max));
       *reinterpret_cast<float4 *>(&ms[lr][sub * 4]) = acc;
       if (m_out && r >= 0) *reinterpret_cast<float4 *>(m_out + r * 64 + sub * 4) = acc;
@@ -348,7 +349,8 @@ __global__ void __launch_bounds__(256, 1) hub_round64_kernel(
     if (h_in && !sh.sol[r]) {
       if (sh.active_ptr)
         acc = hub_gather_row64<TABLE>(sh.active_ptr[q], sh.active_ptr[q + 1], sh.active_cols,
-                                      h_in, ring, hot_rows, pol_hot, pol_cold, deg_src, sh.sol);
+                                      h_in, ring, hot_rows, pol_hot, pol_cold, deg_src,
+                                      sh.active_sol ? sh.active_sol : sh.sol);
       else
         acc = hub_gather_row64<TABLE>(sh.row_ptr[r], sh.row_ptr[r + 1], sh.cols, h_in, ring,
                                       hot_rows, pol_hot, pol_cold, deg_src);
@@ -1104,11 +1106,16 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
     for (int a = 0; a < 4; a++)
 #pragma unroll
       for (int c = 0; c < 4; c++) acc[a][c] = 0.f;
-#pragma unroll 4
+    // fully unrolled: every shared address is one of 9 base registers plus
+    // an immediate (no per-p address arithmetic)
+    const float *tb = &th6T[0][kq * 4];
+    const float *xb[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) xb[j] = xT + ((rq * 4) ^ (j << 2));
+#pragma unroll
     for (int p = 0; p < 64; p++) {
-      const float4 t = *reinterpret_cast<const float4 *>(&th6T[p][kq * 4]);
-      const float4 x4 =
-          *reinterpret_cast<const float4 *>(&xT[p * 64 + ((rq * 4) ^ (((p >> 2) & 7) << 2))]);
+      const float4 t = *reinterpret_cast<const float4 *>(tb + p * 68);
+      const float4 x4 = *reinterpret_cast<const float4 *>(xb[(p >> 2) & 7] + p * 64);
       const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
       for (int a = 0; a < 4; a++) {
@@ -1285,8 +1292,9 @@ static int embed_round_t(const s2v_shard *sh, const void *theta4, const void *ta
                             "at P > 1)");
   const int32_t *deg_src = deg_phys ? deg_phys : sh->rdeg;
   if (sh->active && !(sizeof(T) == 4 && K == 64 && sh->batch == 1 &&
-                      (sh->world == 1 || !sh->active_ptr)))
-    return fail(S2V_EINVAL, "active-row lists need K = 64 fp32, B = 1 (compact CSR: P = 1)");
+                      (sh->world == 1 || !sh->active_ptr || sh->active_sol)))
+    return fail(S2V_EINVAL, "active-row lists need K = 64 fp32, B = 1 (compact CSR at P > 1: "
+                            "active_sol)");
   if (sizeof(T) == 4 && K == 64) {
     static thread_local int *counter = nullptr;
     if (!counter) S2V_CUDA_CHECK(cudaMalloc(&counter, sizeof(int)));

@@ -96,11 +96,19 @@ __global__ void shard_init_kernel(s2v_shard sh, const uint32_t *__restrict__ col
     if (ok) {
       s = sol_phys[(b * sh.world + sh.rank) * sh.rows_max + i];
       const int64_t e1 = sh.row_ptr[r + 1];
-      for (int64_t e = sh.row_ptr[r] + sub; e < e1; e += 8) {
-        const uint32_t c = src[e] & ~S2V_DEAD;
-        const bool dead = s || ((__ldg(sol_bits + (c >> 5)) >> (c & 31)) & 1u);
-        sh.cols[e] = c | (dead ? S2V_DEAD : 0u);
-        cnt += !dead;
+      // four 8-entry steps per iteration: a BA row's ~32 column loads, then
+      // its bitmap lookups, all in flight together
+      for (int64_t e = sh.row_ptr[r] + sub; e < e1; e += 32) {
+        uint32_t c[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) c[q] = e + 8 * q < e1 ? src[e + 8 * q] & ~S2V_DEAD : 0u;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          if (e + 8 * q >= e1) break;
+          const bool dead = s || ((__ldg(sol_bits + (c[q] >> 5)) >> (c[q] & 31)) & 1u);
+          sh.cols[e + 8 * q] = c[q] | (dead ? S2V_DEAD : 0u);
+          cnt += !dead;
+        }
       }
     }
 #pragma unroll
@@ -130,6 +138,17 @@ __global__ void shard_init_kernel(s2v_shard sh, const uint32_t *__restrict__ col
     }
   }
   if (lane == 0 && acc) atomicAdd((unsigned long long *)&sh.residual[acc_b], acc);
+}
+
+// S of every physical row after a group apply: the applied picks (global
+// node ids, identical on every rank) enter S
+__global__ void sol_mark_kernel(s2v_shard sh, PartitionMap pm, const int64_t *__restrict__ picks,
+                                const uint8_t *__restrict__ applied, int d,
+                                uint8_t *__restrict__ sol_all) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= sh.batch * d) return;
+  const int64_t v = picks[t];
+  if (v >= 0 && v < sh.num_nodes && applied[t]) sol_all[phys_of(sh, pm, t / d, v)] = 1;
 }
 
 // Is the edge (row r, neighbour phys q) present and alive?  Row cols are
@@ -526,6 +545,16 @@ int s2v_apply_phase2(const s2v_shard *sh, const int64_t *picks, int d, const int
   return S2V_OK;
 }
 
+int s2v_sol_mark(const s2v_shard *sh, const int64_t *picks, const uint8_t *applied, int d,
+                 uint8_t *sol_all, void *stream) {
+  if (d < 1 || d > 64) return fail(S2V_EINVAL, "group size d=%d outside [1, 64]", d);
+  const int n = sh->batch * d;
+  sol_mark_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(*sh, make_map(*sh), picks,
+                                                                   applied, d, sol_all);
+  S2V_LAUNCH_CHECK();
+  return S2V_OK;
+}
+
 int64_t s2v_active_workspace(int64_t cap) {
   return 3 * ((cap + kCompactChunk - 1) / kCompactChunk) + 3;
 }
@@ -533,9 +562,9 @@ int64_t s2v_active_workspace(int64_t cap) {
 int s2v_active_compact(const s2v_shard *sh, int32_t *list, int64_t *n, int32_t *tmp,
                        int64_t *ws, int64_t cap, int64_t *row_ptr_out, uint32_t *cols_out,
                        void *stream) {
-  // (the list holds local rows: any P; the compact CSR is read only at P = 1)
-  if (sh->batch != 1 || (sh->world != 1 && cols_out))
-    return fail(S2V_EINVAL, "active-row lists need B = 1 (compact CSR: P = 1)");
+  // (the list holds local rows and the CSR physical neighbour rows: any P;
+  // at P > 1 the rounds reading the CSR need shard.active_sol)
+  if (sh->batch != 1) return fail(S2V_EINVAL, "active-row lists need B = 1");
   if ((row_ptr_out == nullptr) != (cols_out == nullptr))
     return fail(S2V_EINVAL, "compact CSR needs both row_ptr_out and cols_out");
   if (cap <= 0) return S2V_OK;

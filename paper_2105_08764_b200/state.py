@@ -264,22 +264,26 @@ class PartitionedState:
 
     @contextlib.contextmanager
     def active_rows(self, rows: torch.Tensor, count: torch.Tensor, colsum_cache=None,
-                    csr=None):
+                    csr=None, sol_all=None):
         """Within the block, forward rounds and the scorer visit only the rows
         of the active list `rows` (int32, count[0] entries, count[1] hub rows
         first; s2v_active_compact) -- the residual rows of an episode.
         colsum_cache: the caller's dict for the incremental global sum
         (s2v_colsum_residual with `last`), valid for fixed parameters.
-        csr: (row_ptr, cols) compact CSR of the list (s2v_active_compact)."""
+        csr: (row_ptr, cols) compact CSR of the list (s2v_active_compact).
+        sol_all: P > 1 with csr -- S of every physical row (s2v_sol_mark)."""
         sh = self._shard
         sh.active, sh.active_n = ptr(rows), ptr(count)
         if csr is not None:
             sh.active_ptr, sh.active_cols = ptr(csr[0]), ptr(csr[1])
+            if sol_all is not None:
+                sh.active_sol = ptr(sol_all)
         self.colsum_cache = colsum_cache
         try:
             yield
         finally:
             sh.active, sh.active_n, sh.active_ptr, sh.active_cols = None, None, None, None
+            sh.active_sol = None
             self.colsum_cache = None
 
     @property

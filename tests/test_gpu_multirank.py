@@ -161,7 +161,8 @@ def test_device_tau_loop_at_p_ranks(p):
 def test_compacted_episode_at_p_ranks(p, monkeypatch):
     """Residual-row compaction at P > 1 (every rank visits only its rows with
     rdeg > 0; the gathered global sum takes dead rows from the h1 table,
-    classified by every rank's e12 rows): the whole episode's pick/apply
+    classified by every rank's e12 rows; each rank's compact CSR tests S of
+    every rank's rows, kept by s2v_sol_mark): the whole episode's pick/apply
     trace equals the P = 1 loop over every row.  R-MAT with isolated nodes."""
     from paper_2105_08764_b200.inference import DeviceEpisode
     monkeypatch.setattr(DeviceEpisode, "COMPACT_MIN_ROWS", 0)
@@ -180,14 +181,15 @@ def test_compacted_episode_at_p_ranks(p, monkeypatch):
                 trace.append((tp.copy(), ta.copy(), te.copy()))
                 if not active.any():
                     break
-            return trace, ep.active_count()
+            return trace, ep.active_count(), getattr(ep, "csr_builds", 0)
         return P.run_workers(comm_size[0], worker)
 
     comm_size = [1]
-    (t_f, _), = run(False)
+    (t_f, _, _), = run(False)
     comm_size[0] = p
     outs = run(True)
-    for trace, n_act in outs:
+    for trace, n_act, csr_builds in outs:
+        assert csr_builds > 0  # the compact CSR was read at P > 1
         assert len(trace) == len(t_f)
         for (a, b, c), (x, y, z) in zip(trace, t_f):
             assert np.array_equal(a, x) and np.array_equal(b, y) and np.array_equal(c, z)
