@@ -453,26 +453,44 @@ int s2v_shard_structure(int64_t n, int P, int64_t rows_max, int64_t rows, const 
 /* ---- handle-level API: library-owned device memory -------
  * Plain host arrays in and out, one call per reference operation; the
  * library allocates and owns every device buffer behind three opaque
- * handles.  Single-rank (world = 1); P > 1 runs through the Python layer's
- * peer-memory transports.  Same kernels, same order, same bits as the Python
- * mirror.  theta is theta1..theta7 packed in PARAM_NAMES order with the
+ * handles.  Node-sharded P > 1: one context per rank, every call below
+ * collective (all ranks call it in the same order, as run_workers' threads
+ * call the reference's API, collective.py:143-195); each rank owns the block
+ * partition_rows(N, P)[rank] of every graph (state.py:36-53), rounds
+ * all-gather every rank's rows of h (policy.py:168) and the global sums are
+ * rank-ordered all-reduces (collective.py:100-117), so every rank returns
+ * the same keys, loss and gradients.  Same kernels, same order, same bits as
+ * the Python mirror.  theta is theta1..theta7 packed in PARAM_NAMES order with the
  * reference's shapes (policy.py:43-113): K, K, K*K, K*K, K*K, K*K, 2K. */
 typedef struct s2v_ctx s2v_ctx;
 typedef struct s2v_graph s2v_graph;
 typedef struct s2v_state s2v_state;
+typedef struct s2v_group s2v_group;
 enum { S2V_OUT_EMBED = 0, S2V_OUT_SOL = 1, S2V_OUT_CAND = 2, S2V_OUT_RDEG = 3,
        S2V_OUT_RESIDUAL = 4, S2V_OUT_SCORES = 5 };
-/* one context per GPU: run_workers' rank thread (collective.py:149-195) */
+/* one context per rank: run_workers' rank thread (collective.py:149-195).
+ * world > 1: ranks join through NCCL; nccl_id = the bytes of
+ * s2v_comm_unique_id made by one rank and shared (one rank per GPU). */
 int s2v_ctx_create(int device, int rank, int world, const void *nccl_id, s2v_ctx **out);
+/* in-process group of `world` thread ranks (WorkerGroup, collective.py:143):
+ * s2v_ctx_create_in_group joins rank `rank` on `device` (any devices, one
+ * GPU may hold several ranks); peers' chunks are copied on the streams
+ * (NVLink P2P between GPUs) and ordered with CUDA events plus a host
+ * rendezvous that fails with S2V_ECOMM after 300 s without a peer
+ * (collective.py:134-139).  Destroy the group after its contexts. */
+int s2v_group_create(int world, s2v_group **out);
+int s2v_group_destroy(s2v_group *g);
+int s2v_ctx_create_in_group(int device, int rank, s2v_group *group, s2v_ctx **out);
 int s2v_ctx_destroy(s2v_ctx *ctx);
 int s2v_ctx_sync(s2v_ctx *ctx);
-/* Graph.csr_arrays() (host row_ptr [n+1], cols [row_ptr[n]]) -> device shard
- * structure (state.py:89-105, 115-122) */
+/* Graph.csr_arrays() (host row_ptr [n+1], cols [row_ptr[n]], the whole
+ * graph on every rank) -> this rank's device shard structure
+ * (state.py:89-105, 115-122) */
 int s2v_graph_upload(s2v_ctx *ctx, int64_t n, const int64_t *row_ptr, const int32_t *cols,
                      s2v_graph **out);
 int s2v_graph_destroy(s2v_graph *g);
 /* PartitionedState(graphs, part, solutions) (state.py:56-111): sol host
- * [B][N] 0/1 bytes or NULL */
+ * [B][N] 0/1 bytes over every node, or NULL */
 int s2v_state_create(s2v_ctx *ctx, s2v_graph *const *graphs, int B, const uint8_t *sol,
                      s2v_state **out);
 int s2v_state_destroy(s2v_state *st);
@@ -496,7 +514,9 @@ int s2v_loss_grad(s2v_ctx *ctx, s2v_state *st, s2v_dtype dt, const void *theta, 
 int s2v_adam_update(s2v_ctx *ctx, s2v_dtype dt, void *params, const void *grads, void *m,
                     void *v, int64_t n, int step, double lr, double beta1, double beta2,
                     double eps);
-/* host copy of a state array (S2V_OUT_*) */
+/* host copy of a state array (S2V_OUT_*): EMBED [B][N][K] (every node);
+ * SOL, CAND [B][rows] uint8, RDEG [B][rows] int32, SCORES [B][rows] over
+ * this rank's rows; RESIDUAL [B] alive local entries */
 int s2v_copy_out(s2v_ctx *ctx, const s2v_state *st, int what, void *host);
 
 /* ---- graph ingestion (graphs.py:125-157) --------------------------------- */

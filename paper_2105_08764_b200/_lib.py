@@ -149,6 +149,9 @@ _SIGNATURES = {
     # above)
     "s2v_ctx_create": ([_I, _I, _I, _P, ctypes.POINTER(ctypes.c_void_p)], _I),
     "s2v_ctx_destroy": ([_P], _I),
+    "s2v_group_create": ([_I, ctypes.POINTER(ctypes.c_void_p)], _I),
+    "s2v_group_destroy": ([_P], _I),
+    "s2v_ctx_create_in_group": ([_I, _I, _P, ctypes.POINTER(ctypes.c_void_p)], _I),
     "s2v_ctx_sync": ([_P], _I),
     "s2v_graph_upload": ([_P, _I64, _P, _P, ctypes.POINTER(ctypes.c_void_p)], _I),
     "s2v_graph_destroy": ([_P], _I),

@@ -1,9 +1,11 @@
 """Child process of tests/test_gpu_handle_abi.py: drives libs2v.so through
 the handle-level C ABI (include/s2v.h, s2v_ctx / s2v_graph / s2v_state) with
 plain ctypes + numpy -- torch is never imported -- against the reference's
-golden fixtures.  Prints "OK <checks>" on success."""
+golden fixtures, single-rank and node-sharded (P = 2, 3 thread ranks of
+one in-process group sharing the GPU).  Prints "OK <checks>" on success."""
 import ctypes
 import sys
+import threading
 from pathlib import Path
 
 import numpy as np
@@ -26,7 +28,9 @@ lib.s2v_loss_grad.argtypes = [P, P, I, P, I, I, P, P, P, ctypes.POINTER(ctypes.c
 lib.s2v_adam_update.argtypes = [P, I, P, P, P, P, I64, I, ctypes.c_double, ctypes.c_double,
                                 ctypes.c_double, ctypes.c_double]
 lib.s2v_copy_out.argtypes = [P, P, I, P]
-for f in ("s2v_graph_destroy", "s2v_state_destroy", "s2v_ctx_destroy"):
+lib.s2v_group_create.argtypes = [I, ctypes.POINTER(P)]
+lib.s2v_ctx_create_in_group.argtypes = [I, I, P, ctypes.POINTER(P)]
+for f in ("s2v_graph_destroy", "s2v_state_destroy", "s2v_ctx_destroy", "s2v_group_destroy"):
     getattr(lib, f).argtypes = [P]
 NAMES = [f"theta{i}" for i in range(1, 8)]
 
@@ -72,14 +76,17 @@ def scale_error(x, y):
     return float(np.abs(x - y).max() / max(np.abs(x).max(), np.abs(y).max(), 1e-9))
 
 
-def main():
-    assert "torch" not in sys.modules
-    ctx = P()
-    ok(lib.s2v_ctx_create(0, 0, 1, None, ctypes.byref(ctx)), "ctx_create")
-    checks = 0
-    # -- forward: embeddings, g, scores bit for bit (fwd_ba1000_k64_l5) ---
+def part(n, world, rank):
+    """partition_rows(n, world)[rank] (state.py:36-53): (start, rows)."""
+    base, extra = divmod(n, world)
+    return rank * base + min(rank, extra), base + (1 if rank < extra else 0)
+
+
+def forward_checks(ctx, rank, world):
+    """fwd_ba1000_k64_l5: embeddings, g, scores bit for bit; the apply errors."""
     z = np.load(GOLD / "fwd_ba1000_k64_l5.npz")
     n, K, L = int(z["n"]), int(z["K"]), int(z["L"])
+    r0, rows = part(n, world, rank)
     g = upload(ctx, n, int(z["m"]), int(z["seed"]))
     st = P()
     graphs = (P * 1)(g)
@@ -96,53 +103,66 @@ def main():
     keys = np.empty((1, 8, 2), np.uint64)
     cnt = np.empty(1, np.int64)
     ok(lib.s2v_score_topk(ctx, st, 8, a(keys), a(cnt)), "score_topk")
-    sc = np.empty(n, np.float32)
+    sc = np.empty(rows, np.float32)
     ok(lib.s2v_copy_out(ctx, st, 5, a(sc)), "copy_out scores")
-    cand = np.empty(n, np.uint8)
+    cand = np.empty(rows, np.uint8)
     ok(lib.s2v_copy_out(ctx, st, 2, a(cand)), "copy_out cand")
-    assert np.array_equal(cand, z["cand"]), "cand"
+    assert np.array_equal(cand, z["cand"][r0:r0 + rows]), "cand"
     c = cand.astype(bool)
-    assert np.array_equal(sc[c], z["scores"][c]), "scores"
-    assert int(cnt[0]) == int(c.sum())
-    top = np.flatnonzero(c)[np.argsort(-z["scores"][c], kind="stable")][:8]
+    assert np.array_equal(sc[c], z["scores"][r0:r0 + rows][c]), "scores"
+    call = z["cand"].astype(bool)
+    assert int(cnt[0]) == int(call.sum())
+    top = np.flatnonzero(call)[np.argsort(-z["scores"][call], kind="stable")][:8]
     assert np.array_equal((~keys[0, :, 1]).astype(np.int64), top), "top-8 keys"
-    checks += 6
-    # apply: the reference's errors before anything is applied
+    # apply: the reference's errors before anything is applied (at P > 1 the
+    # owner's verdict reaches every rank)
     v = np.array([int(top[0])], np.int64)
     ok(lib.s2v_apply(ctx, st, a(v), 1, None, None), "apply")
     rc = lib.s2v_apply(ctx, st, a(v), 1, None, None)
     assert rc == 2 and b"already in the solution" in lib.s2v_last_error()
-    ok(lib.s2v_copy_out(ctx, st, 1, a(cand)), "copy_out sol")
-    assert cand[v[0]] == 1
-    checks += 1
+    sol_l = np.empty(rows, np.uint8)
+    ok(lib.s2v_copy_out(ctx, st, 1, a(sol_l)), "copy_out sol")
+    if r0 <= v[0] < r0 + rows:
+        assert sol_l[v[0] - r0] == 1
     lib.s2v_state_destroy(st)
     lib.s2v_graph_destroy(g)
-    # -- full adaptive solve: cover, evaluations, skips (solve_ba1000_k64_l5) --
+    return 7
+
+
+def solve_checks(ctx):
+    """solve_ba1000_k64_l5: the whole adaptive trajectory."""
     z = np.load(GOLD / "solve_ba1000_k64_l5.npz")
     g = upload(ctx, 1000, 4, 0)
     st = P()
     ok(lib.s2v_state_create(ctx, (P * 1)(g), 1, None, ctypes.byref(st)), "state_create")
     theta = init_theta(int(z["K"]), int(z["L"]), int(z["pseed"]))
+    keys = np.empty((1, 8, 2), np.uint64)
+    cnt = np.empty(1, np.int64)
     cover, evals, skipped = [], 0, 0
-    res = np.array([1], np.int64)
-    while res[0] > 0:
+    while True:
         ok(lib.s2v_embed(ctx, st, 0, a(theta), int(z["K"]), int(z["L"])), "embed")
         ok(lib.s2v_score_topk(ctx, st, 8, a(keys), a(cnt)), "score_topk")
         c = int(cnt[0])
+        if c == 0:
+            break
         d = next((dd for f, dd in ((0.5, 8), (0.25, 4), (0.125, 2)) if c > f * 1000), 1)
         d = min(d, c)  # SelectionSchedule.adaptive (inference.py:54-58)
         picks = np.ascontiguousarray((~keys[0, :d, 1]).astype(np.int64)[None])
         applied = np.zeros((1, d), np.uint8)
-        ok(lib.s2v_apply(ctx, st, a(picks), d, a(applied), a(res)), "apply")
+        ok(lib.s2v_apply(ctx, st, a(picks), d, a(applied), None), "apply")
         cover += [int(v) for v, f in zip(picks[0], applied[0]) if f]
         skipped += int(d - applied.sum())
         evals += 1
     assert sorted(cover) == z["covers"].tolist(), "cover"
     assert evals == int(z["evals"][0]) and skipped == int(z["skipped"][0])
-    checks += 2
     lib.s2v_state_destroy(st)
     lib.s2v_graph_destroy(g)
-    # -- training step: grads, loss, Adam (train_ba1000_b4_k64_l5) ----------
+    return 2
+
+
+def train_checks(ctx):
+    """train_ba1000_b4_k64_l5: loss, grads, Adam over tau steps.  Returns
+    the first step's gradients (replicas must agree at P > 1)."""
     z = np.load(GOLD / "train_ba1000_b4_k64_l5.npz")
     n, B, K, L, tau = (int(z[k]) for k in ("n", "B", "K", "L", "tau"))
     gl = [upload(ctx, n, int(z["m"]), 100 + i) for i in range(B)]
@@ -156,11 +176,13 @@ def main():
     loss = ctypes.c_double()
     acts = np.ascontiguousarray(z["actions"], np.int64)
     tg = np.ascontiguousarray(z["targets"], np.float32)
+    first = None
     for it in range(tau):
         ok(lib.s2v_loss_grad(ctx, st, 0, a(theta), K, L, a(acts), a(tg), a(grads),
                              ctypes.byref(loss)), "loss_grad")
         assert abs(loss.value - z["losses"][it]) <= 1e-4 * abs(z["losses"][it]), "loss"
         if it == 0:
+            first = (loss.value, grads.copy())
             g0 = np.concatenate([z[f"g0_{k}"].reshape(-1) for k in NAMES])
             off = 0
             for k in NAMES:
@@ -181,11 +203,58 @@ def main():
     rc = lib.s2v_adam_update(ctx, 0, a(theta), a(bad), a(m), a(v), theta.size, tau + 1, 1e-5,
                              0.9, 0.999, 1e-8)
     assert rc == 5 and np.array_equal(theta, before), "non-finite rejection"
-    checks += 4
     lib.s2v_state_destroy(st)
     for x in gl:
         lib.s2v_graph_destroy(x)
+    return 4, first
+
+
+def run_ranks(world, fn):
+    """fn(ctx, rank) on `world` thread ranks of one in-process group (all on
+    GPU 0); returns the per-rank results, raising the first failure."""
+    grp = P()
+    ok(lib.s2v_group_create(world, ctypes.byref(grp)), "group_create")
+    out, errs = [None] * world, []
+
+    def body(rank):
+        ctx = P()
+        try:
+            ok(lib.s2v_ctx_create_in_group(0, rank, grp, ctypes.byref(ctx)), "ctx_create_in_group")
+            out[rank] = fn(ctx, rank)
+        except BaseException as e:  # noqa: BLE001 (reported by the caller)
+            errs.append(f"rank {rank}: {e!r}")
+        finally:
+            lib.s2v_ctx_destroy(ctx)
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    lib.s2v_group_destroy(grp)
+    if errs:
+        raise AssertionError("; ".join(errs))
+    return out
+
+
+def main():
+    assert "torch" not in sys.modules
+    ctx = P()
+    ok(lib.s2v_ctx_create(0, 0, 1, None, ctypes.byref(ctx)), "ctx_create")
+    checks = forward_checks(ctx, 0, 1) + solve_checks(ctx)
+    c, (loss1, grads1) = train_checks(ctx)
+    checks += c
     lib.s2v_ctx_destroy(ctx)
+    # node-sharded: the same goldens at P = 2, 3 thread ranks, every rank
+    # returning the same keys, trajectory, loss and gradients
+    for world in (2, 3):
+        checks += sum(run_ranks(world, lambda c, r: forward_checks(c, r, world)))
+        checks += sum(run_ranks(world, lambda c, r: solve_checks(c)))
+        res = run_ranks(world, lambda c, r: train_checks(c))
+        for c, (loss, grads) in res:
+            checks += c
+            assert loss == res[0][1][0] and np.array_equal(grads, res[0][1][1]), "replicas"
+            assert abs(loss - loss1) <= 1e-6 * abs(loss1)
+            assert scale_error(grads, grads1) < 1e-5, "P-invariant gradients"
     assert "torch" not in sys.modules
     print("OK", checks)
 
