@@ -8,7 +8,12 @@ avoid its 216 s pure-Python generation the bit-identical native generator's
 edge list is fed to the reference's own Graph (tests/test_oracle.py pins
 the generator against the reference at smaller sizes).  Run here only:
 
-    OPENBLAS_CORETYPE=SkylakeX python oracle/make_golden_full.py [infer|train]
+    OPENBLAS_CORETYPE=SkylakeX python oracle/make_golden_full.py [infer|mid|train]
+
+`mid` is SURVEY.md 8(d)'s mid-episode cfg3 state: S_mid = a seeded random
+35% of the nodes (default_rng(11)), built on both sides with
+PartitionedState(..., solutions=S_mid), then one forward and the first
+adaptive steps from it.
 """
 from __future__ import annotations
 
@@ -41,8 +46,11 @@ def main(which: str):
     params = R.PolicyParams.initialize(64, 5, seed=0)
     comm = R.WorkerGroup(1).comm(0)
     part = R.partition_rows(g.num_nodes, 1)[0]
-    if which == "infer":
-        st = R.PartitionedState([g], part)
+    sol = None
+    if which == "mid":
+        sol = (np.random.default_rng(11).random(g.num_nodes) < 0.35).astype(np.uint8)[None]
+    if which in ("infer", "mid"):
+        st = R.PartitionedState([g], part, solutions=sol)
         t0 = time.time()
         emb = R.embed_forward(st, params, comm)
         sc = R.q_forward(emb, st.cand, params, comm)
@@ -50,7 +58,10 @@ def main(which: str):
         u1 = (gsum[None] @ params.theta5.T)[0]
         h = np.ascontiguousarray(emb[0].T)
         print("forward", f"{time.time() - t0:.1f}s", flush=True)
-        out = {"config": "BA(2000000,16,0), K=64, L=5, params seed 0, S = {}",
+        out = {"config": "BA(2000000,16,0), K=64, L=5, params seed 0, " + (
+                   "S = {}" if sol is None else
+                   "S_mid = default_rng(11).random(N) < 0.35 (%d nodes)" % int(sol.sum())),
+               "residual": int(st.local_residual[0]),
                "h_sha256": digest(h), "scores_sha256": digest(sc[0]),
                "cand_sha256": digest(st.cand[0]), "g": gsum.tolist(), "u1": u1.tolist(),
                "h_row0": h[0].tolist(), "scores_head": sc[0][:16].tolist()}
@@ -64,9 +75,9 @@ def main(which: str):
             return res
         inf.select_top_d = hooked
         try:
-            st2 = R.PartitionedState([g], part)
+            st2 = R.PartitionedState([g], part, solutions=sol)
             sched = R.SelectionSchedule.adaptive()
-            for _ in range(3):
+            for _ in range(3 if sol is None else 2):
                 t0 = time.time()
                 e = R.embed_forward(st2, params, comm)
                 s2 = R.q_forward(e, st2.cand, params, comm)
@@ -83,7 +94,8 @@ def main(which: str):
         finally:
             inf.select_top_d = orig
         out["first_steps_picks"] = picks_log
-        (OUT / "full_cfg3_infer.json").write_text(json.dumps(out))
+        (OUT / ("full_cfg3_infer.json" if sol is None else "full_cfg3_mid.json")).write_text(
+            json.dumps(out))
     else:
         # cfg4 at the CPU oracle's size: B=2 tuples, tau=1
         import graphrl.agent as ag

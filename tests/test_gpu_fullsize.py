@@ -87,3 +87,53 @@ def test_cfg4_training_step_matches_reference(ba2m):
     # is held to 1e-4 against the reference's own value
     for k in P.PARAM_NAMES:
         assert scale_error(grads[k], np.asarray(gold["grads"][k])).max() < 1e-4, k
+
+
+def test_cfg3_mid_episode_state_matches_reference(ba2m):
+    """SURVEY.md 8(d) cfg3 S_mid: a seeded random 35% of the nodes in S,
+    built on both sides with PartitionedState(..., solutions=S_mid).  The
+    residual, candidate set, embedding and score bytes hash to the
+    reference's; the first adaptive groups match pick for pick through
+    solve_step and through the device episode loop (whose residual-row
+    compaction and compact CSR switch on at this residual)."""
+    path = GOLD / "full_cfg3_mid.json"
+    if not path.exists():
+        pytest.skip("full-size golden not generated")
+    gold = json.loads(path.read_text())
+    params = P.PolicyParams.initialize(64, 5, seed=0)
+    n = ba2m.num_nodes
+    sol = (np.random.default_rng(11).random(n) < 0.35).astype(np.uint8)[None]
+    from paper_2105_08764_b200.inference import DeviceEpisode
+    from paper_2105_08764_b200.policy import _global_sum
+
+    def worker(comm):
+        part = P.partition_rows(n, 1)[0]
+        st = P.PartitionedState([ba2m], part, solutions=sol)
+        residual = int(st.local_residual[0])
+        emb = P.embed_forward(st, params, comm)
+        h = emb.local_rows()[0].to("cpu").numpy()
+        sc = P.q_forward(emb, st.cand, params, comm)[0]
+        g = _global_sum(emb)[0]
+        cand = st.cand[0].copy()
+        sched = P.SelectionSchedule.adaptive()
+        steps = []
+        for _ in range(len(gold["first_steps_picks"])):
+            picks, _ = P.inference.solve_step(st, params, comm, sched, np.array([True]))
+            steps.append([int(v) for v in picks[0] if v >= 0])
+        st.release()
+        st2 = P.PartitionedState([ba2m], part, solutions=sol)
+        ep = DeviceEpisode(st2, params, comm, sched, len(gold["first_steps_picks"]),
+                           use_graph=False)
+        tp, _, _, _ = ep.run_chunk()
+        ep_steps = [[int(v) for v in row if v >= 0] for row in tp]
+        return residual, h, sc, g, cand, steps, ep_steps, ep.compact, ep._mode
+    residual, h, sc, g, cand, steps, ep_steps, compact, mode = P.run_workers(1, worker)[0]
+    assert residual == gold["residual"]
+    assert _sha(cand) == gold["cand_sha256"]
+    assert np.array_equal(g, np.asarray(gold["g"], np.float32))
+    assert np.array_equal(h[0], np.asarray(gold["h_row0"], np.float32))
+    assert _sha(h) == gold["h_sha256"]
+    assert _sha(sc) == gold["scores_sha256"]
+    assert steps == gold["first_steps_picks"]
+    assert ep_steps == gold["first_steps_picks"]
+    assert compact and mode[0] and mode[1]  # the list and its compact CSR were read

@@ -257,6 +257,7 @@ def test_incremental_episode_at_p_ranks(p, inc_cap, monkeypatch):
 
     (t_f, _), = run(1, False)
     monkeypatch.setattr(DeviceEpisode, "INC_RATIO", 1e9)
+    monkeypatch.setattr(DeviceEpisode, "INC_SLOWER", float("inf"))  # no timing fallback
     monkeypatch.setattr(DeviceEpisode, "LIST_FRAC", 1.0)
     monkeypatch.setattr(DeviceEpisode, "INC_CAP", inc_cap)
     if inc_cap == 0.0:

@@ -30,6 +30,10 @@ while active.any():
         ep.resize(16, use_graph=True)
         tail = True
         print("tail mode at eval", evals, flush=True)
+    elif tail and not ep._mode[2] and ep.active_count() > tail_rows and ep.chunk != 1:
+        ep.resize(1, use_graph=False)  # as solve(): the incremental trial fell back
+        tail = False
+        print("incremental trial fell back at eval", evals, flush=True)
     tp, ta, te, active = ep.run_chunk()
     evals += int(te.sum())
     while dumps and evals >= dumps[0]:
@@ -41,7 +45,8 @@ while active.any():
         print(f"t {now:7.1f}s evals {evals:7d} active {ep.active_count():8d} alive "
               f"{int(st.residual_d.sum().item()):10d} d {d} "
               f"{(now - last_t) / max(evals - last_e, 1) * 1e3:.3f} ms/eval inc {int(ep._mode[2])} "
-              f"overflow {int(ep.front_meta[2].item()) if ep.front is not None else -1}", flush=True)
+              f"overflow {int(ep.front_meta[2].item()) if ep.front is not None else -1} "
+              f"fallbacks {ep.inc_fallbacks}", flush=True)
         last_t, last_e = now, evals
     if now > budget:
         break
