@@ -125,7 +125,7 @@ def test_cfg3_mid_episode_state_matches_reference(ba2m):
         ep = DeviceEpisode(st2, params, comm, sched, len(gold["first_steps_picks"]),
                            use_graph=False)
         tp, _, _, _ = ep.run_chunk()
-        ep_steps = [[int(v) for v in row if v >= 0] for row in tp]
+        ep_steps = [[int(v) for v in row if v >= 0] for row in tp[:, 0]]
         return residual, h, sc, g, cand, steps, ep_steps, ep.compact, ep._mode
     residual, h, sc, g, cand, steps, ep_steps, compact, mode = P.run_workers(1, worker)[0]
     assert residual == gold["residual"]
