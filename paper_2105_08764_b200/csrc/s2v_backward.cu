@@ -258,16 +258,6 @@ __global__ void __launch_bounds__(kBwdThreads) param_grads_kernel(
 constexpr int kEinRows = 1024;
 constexpr int kEinStages = 3;
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
 template <class T>
 __global__ void __launch_bounds__(256) theta2_einsum_kernel(const T *__restrict__ t2c,
                                                             int64_t rows, int K,

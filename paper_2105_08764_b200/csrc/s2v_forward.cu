@@ -1002,12 +1002,21 @@ __global__ void __launch_bounds__(256) score_generic_kernel(
     atomicAdd((unsigned long long *)&counts[b], s_count);
 }
 
-// K = 64 fp32 scorer: tiles of 64 rows; u2 = theta6 (h*cand) as a 4x4
-// register-tiled FMA chain (p = 0..63 per output), then one thread per row
-// runs the sequential theta7 contraction (mul then add, j = 0..127).
-constexpr int kScoreTile = 64;
+// K = 64 fp32 scorer: 128-row tiles.  The next tile's rows are copied into a
+// row-major staging buffer by cp.async (no registers held) while the current
+// tile is projected; each thread then moves the rows it copied into the
+// transposed xT[p][row].  u2 = theta6 h as an 8-row x 4-k register-tiled FMA
+// chain (p = 0..63 per output, the order numpy's sgemm uses; 3 shared loads
+// per 32 FMAs), then one thread per row runs the sequential theta7
+// contraction (mul then add, j = 0..127).  The candidate mask of
+// q_forward's theta6 (h * cand) is applied to u2 instead of h: for a
+// non-candidate row every x_p is +-0 (finite h) or NaN, so every chain of
+// fl(h * 0) gives exactly +0 -- or NaN if the row holds a non-finite value
+// -- which is what the masked chain computes, bit for bit.
+constexpr int kScoreTile = 128;
+constexpr size_t kScoreSmem = sizeof(float) * (64 * 68 + kScoreTile * 64 + kScoreTile * 68);
 
-__global__ void __launch_bounds__(256, 3) score64_kernel(
+__global__ void __launch_bounds__(256, 2) score64_kernel(
     s2v_shard sh, const float *__restrict__ h, const float *__restrict__ u1,
     const float *__restrict__ theta6, const float *__restrict__ theta7,
     const uint8_t *__restrict__ cand_override, int mode, float *__restrict__ scores,
@@ -1015,20 +1024,22 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
     float *__restrict__ prod_cache = nullptr, int emit = 1) {
   // prod_cache (nullable, [rows][64]): keep each row's fl(relu(u2) * theta7)
   // terms for score_sum64_kernel; emit = 0: only fill the cache
-  __shared__ __align__(16) float th6T[64][68];           // th6T[p][k] = theta6[k][p]
-  // xT[p][row] = h[row][p]*c; after the projection the same storage holds
-  // prod[row][k] = fl(relu(u2) * theta7), and at the end the key lists
-  __shared__ __align__(16) float xbuf[kScoreTile * 68];
-  float *xT = xbuf;  // [64 p][64 rows], 4-row groups swizzled
-  float(*prod)[65] = reinterpret_cast<float(*)[65]>(xbuf);
+  extern __shared__ __align__(16) float score_smem[];
+  float(*th6T)[68] = reinterpret_cast<float(*)[68]>(score_smem);  // th6T[p][k] = theta6[k][p]
+  float *stage = score_smem + 64 * 68;                             // [128 rows][64], cp.async
+  // xT[p][row] (4-row groups XOR-swizzled by (p >> 2) & 7); after the
+  // projection the same storage holds prod[row][k] = fl(relu(u2) * theta7),
+  // and at the end the key lists
+  float *xT = stage + kScoreTile * 64;
+  float(*prod)[68] = reinterpret_cast<float(*)[68]>(xT);
   __shared__ float s_t7[64];
-  __shared__ uint8_t s_c[kScoreTile];
+  __shared__ uint8_t s_c[kScoreTile], s_nf[kScoreTile];
   __shared__ int32_t s_i[kScoreTile];
   __shared__ float s_s0;
   __shared__ unsigned long long s_count;
-  Key *s_keys = reinterpret_cast<Key *>(xbuf);
+  Key *s_keys = reinterpret_cast<Key *>(xT);
   const int b = blockIdx.y, tid = threadIdx.x;
-  // 64-row tiles are dealt to blocks round-robin (tile t -> block t mod
+  // 128-row tiles are dealt to blocks round-robin (tile t -> block t mod
   // gridDim.x), so a short active list still spreads over every block
   const int64_t lim = sh.active ? sh.active_n[0] : sh.num_rows;
   if ((int64_t)blockIdx.x * kScoreTile >= lim) {
@@ -1036,6 +1047,29 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
     if (tid < kTopK) block_keys[((int64_t)b * gridDim.x + blockIdx.x) * kTopK + tid] = null_key();
     return;
   }
+  const int64_t i0 = (int64_t)blockIdx.x * kScoreTile;
+  const int64_t tstride = (int64_t)gridDim.x * kScoreTile;
+  const int64_t i1 = lim;
+  const int64_t base_r = (int64_t)b * sh.num_rows;
+  const int64_t base_phys = ((int64_t)b * sh.world + sh.rank) * sh.rows_max;
+  // copy role: chunk e = tid + 256 q (q = 0..7) is row (tid >> 4) + 16 q,
+  // float4 column c16 = tid & 15
+  const int c16 = tid & 15, crow = tid >> 4;
+  auto issue = [&](int64_t t0) {
+    if (t0 < i1) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const int row = crow + 16 * q;
+        const int64_t j = t0 + row;
+        if (j < i1) {
+          const int64_t i = sh.active ? sh.active[j] : j;
+          cp_async16(stage + row * 64 + c16 * 4, h + (base_phys + i) * 64 + c16 * 4);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  issue(i0);
   for (int idx = tid; idx < 64 * 64; idx += 256) th6T[idx % 64][idx / 64] = theta6[idx];
   if (tid < 64) s_t7[tid] = theta7[64 + tid];
   if (tid == 0) {
@@ -1048,105 +1082,97 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
 #pragma unroll
   for (int q = 0; q < kTopK; q++) top[q] = null_key();
   unsigned long long cnt = 0;
-  // positions [i0, i1) of this block: local rows, or entries of the active
-  // list (B = 1) when set -- rows off the list have rdeg = 0, not candidates
-  const int64_t i0 = (int64_t)blockIdx.x * kScoreTile;
-  const int64_t tstride = (int64_t)gridDim.x * kScoreTile;
-  const int64_t i1 = lim;
-  const int64_t base_r = (int64_t)b * sh.num_rows;
-  const int64_t base_phys = ((int64_t)b * sh.world + sh.rank) * sh.rows_max;
+  // compute role: rows rq*8 .. rq*8+7, k = kq*4 .. kq*4+3
   const int kq = tid & 15, rq = tid >> 4;
-  // software pipeline: the next tile's rows are loaded into registers while
-  // the current tile is projected
-  float4 pre[4];
-  uint8_t pre_c[4];
-  int32_t pre_i[4];
-  auto load_tile = [&](int64_t t0) {
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const int e = tid + q * 256;
-      const int row = e >> 4, k4 = e & 15;
-      const int64_t j = t0 + row;
-      pre[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      pre_c[q] = 0;
-      pre_i[q] = -1;
-      if (t0 < i1 && j < i1) {
-        const int64_t i = sh.active ? sh.active[j] : j;
-        pre_i[q] = (int32_t)i;
-        pre_c[q] = cand_override ? cand_override[base_r + i] : sh.cand[base_r + i];
-        pre[q] = ldg_f4_pol(h + (base_phys + i) * 64 + k4 * 4, l2_policy_first());
-      }
-    }
-  };
-  load_tile(i0);
   for (int64_t t0 = i0; t0 < i1; t0 += tstride) {
-    __syncthreads();
-    // x = h * cand (fl(h*1) = h, fl(h*0) = +-0)
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const int e = tid + q * 256;
-      const int row = e >> 4, k4 = e & 15;
-      const float c = pre_c[q] ? 1.f : 0.f;
-      if (k4 == 0) {
-        s_c[row] = pre_c[q];
-        s_i[row] = pre_i[q];
+    // this tile's row ids and candidate flags (one thread per row)
+    if (tid < kScoreTile) {
+      const int64_t j = t0 + tid;
+      int32_t i = -1;
+      uint8_t c = 0;
+      if (j < i1) {
+        i = (int32_t)(sh.active ? sh.active[j] : j);
+        c = cand_override ? cand_override[base_r + i] : sh.cand[base_r + i];
       }
-      // transposed, 4-row groups XOR-swizzled by (p >> 2) & 7: the
-      // projection reads 4 rows of one p as one float4 (2-way store conflicts)
-      const int rsw = row ^ ((k4 & 7) << 2);
-      xT[(k4 * 4 + 0) * 64 + rsw] = __fmul_rn(pre[q].x, c);
-      xT[(k4 * 4 + 1) * 64 + rsw] = __fmul_rn(pre[q].y, c);
-      xT[(k4 * 4 + 2) * 64 + rsw] = __fmul_rn(pre[q].z, c);
-      xT[(k4 * 4 + 3) * 64 + rsw] = __fmul_rn(pre[q].w, c);
+      s_i[tid] = i;
+      s_c[tid] = c;
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // (also: the previous tile's prod / keys fully consumed)
+    // rows this thread copied -> xT; a row's non-finite flag over its 16 lanes
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int row = crow + 16 * q;
+      const float4 v = *reinterpret_cast<const float4 *>(stage + row * 64 + c16 * 4);
+      const int rsw = row ^ ((c16 & 7) << 2);
+      xT[(c16 * 4 + 0) * kScoreTile + rsw] = v.x;
+      xT[(c16 * 4 + 1) * kScoreTile + rsw] = v.y;
+      xT[(c16 * 4 + 2) * kScoreTile + rsw] = v.z;
+      xT[(c16 * 4 + 3) * kScoreTile + rsw] = v.w;
+      unsigned nf = !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+      nf |= __shfl_xor_sync(0xffffffffu, nf, 1);
+      nf |= __shfl_xor_sync(0xffffffffu, nf, 2);
+      nf |= __shfl_xor_sync(0xffffffffu, nf, 4);
+      nf |= __shfl_xor_sync(0xffffffffu, nf, 8);
+      if (c16 == 0) s_nf[row] = (uint8_t)nf;
     }
     __syncthreads();
-    load_tile(t0 + tstride);
-    float acc[4][4];
+    issue(t0 + tstride);  // the stage is free again
+    float acc[8][4];
 #pragma unroll
-    for (int a = 0; a < 4; a++)
+    for (int a = 0; a < 8; a++)
 #pragma unroll
       for (int c = 0; c < 4; c++) acc[a][c] = 0.f;
-    // fully unrolled: every shared address is one of 9 base registers plus
-    // an immediate (no per-p address arithmetic)
     const float *tb = &th6T[0][kq * 4];
+    // rows rq*8 .. +3 and rq*8+4 .. +7 of p sit at xT[p][(rq*8) ^ (g << 2)]
+    // and at that offset ^ 4, g = (p >> 2) & 7
     const float *xb[8];
 #pragma unroll
-    for (int j = 0; j < 8; j++) xb[j] = xT + ((rq * 4) ^ (j << 2));
+    for (int g = 0; g < 8; g++) xb[g] = xT + ((rq * 8) ^ (g << 2));
+#pragma unroll 1
+    for (int p0 = 0; p0 < 64; p0 += 32) {  // (32-way unroll: g is a constant)
 #pragma unroll
-    for (int p = 0; p < 64; p++) {
-      const float4 t = *reinterpret_cast<const float4 *>(tb + p * 68);
-      const float4 x4 = *reinterpret_cast<const float4 *>(xb[(p >> 2) & 7] + p * 64);
-      const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
+      for (int u = 0; u < 32; u++) {
+        const int p = p0 + u, g = (u >> 2) & 7;
+        const float4 t = *reinterpret_cast<const float4 *>(tb + p * 68);
+        const float4 xa = *reinterpret_cast<const float4 *>(xb[g] + p * kScoreTile);
+        const float4 xc = *reinterpret_cast<const float4 *>(xb[g ^ 1] + p * kScoreTile);
+        const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xc.x, xc.y, xc.z, xc.w};
 #pragma unroll
-      for (int a = 0; a < 4; a++) {
-        const float xr = xv[a];
-        acc[a][0] = __fmaf_rn(t.x, xr, acc[a][0]);
-        acc[a][1] = __fmaf_rn(t.y, xr, acc[a][1]);
-        acc[a][2] = __fmaf_rn(t.z, xr, acc[a][2]);
-        acc[a][3] = __fmaf_rn(t.w, xr, acc[a][3]);
+        for (int a = 0; a < 8; a++) {
+          acc[a][0] = __fmaf_rn(t.x, xv[a], acc[a][0]);
+          acc[a][1] = __fmaf_rn(t.y, xv[a], acc[a][1]);
+          acc[a][2] = __fmaf_rn(t.z, xv[a], acc[a][2]);
+          acc[a][3] = __fmaf_rn(t.w, xv[a], acc[a][3]);
+        }
       }
     }
     __syncthreads();  // xT fully consumed before prod overwrites it
+    const float4 t7 = *reinterpret_cast<const float4 *>(&s_t7[kq * 4]);
 #pragma unroll
-    for (int a = 0; a < 4; a++)
-#pragma unroll
-      for (int c = 0; c < 4; c++)
-        prod[rq * 4 + a][kq * 4 + c] = __fmul_rn(relu(acc[a][c]), s_t7[kq * 4 + c]);
-    if (prod_cache) {
-#pragma unroll
-      for (int a = 0; a < 4; a++) {
-        const int32_t i = s_i[rq * 4 + a];
-        if (i >= 0)
-          *reinterpret_cast<float4 *>(prod_cache + (int64_t)i * 64 + kq * 4) =
-              make_float4(prod[rq * 4 + a][kq * 4 + 0], prod[rq * 4 + a][kq * 4 + 1],
-                          prod[rq * 4 + a][kq * 4 + 2], prod[rq * 4 + a][kq * 4 + 3]);
-      }
+    for (int a = 0; a < 8; a++) {
+      const int row = rq * 8 + a;
+      // q_forward's theta6 (h * cand): a non-candidate row's chains are +0
+      // (NaN if the row is not finite)
+      const bool c = s_c[row] != 0;
+      const float z = s_nf[row] ? __int_as_float(0x7fffffff) : 0.f;
+      const float4 pv = make_float4(__fmul_rn(relu(c ? acc[a][0] : z), t7.x),
+                                    __fmul_rn(relu(c ? acc[a][1] : z), t7.y),
+                                    __fmul_rn(relu(c ? acc[a][2] : z), t7.z),
+                                    __fmul_rn(relu(c ? acc[a][3] : z), t7.w));
+      *reinterpret_cast<float4 *>(&prod[row][kq * 4]) = pv;
+      const int32_t i = s_i[row];
+      if (prod_cache && i >= 0)
+        *reinterpret_cast<float4 *>(prod_cache + (int64_t)i * 64 + kq * 4) = pv;
     }
     __syncthreads();
     if (emit && tid < kScoreTile && t0 + tid < i1) {
       float sc = s_s0;
-#pragma unroll 16
-      for (int k = 0; k < 64; k++) sc = __fadd_rn(sc, prod[tid][k]);
+#pragma unroll
+      for (int k4 = 0; k4 < 16; k4++) {
+        const float4 v = *reinterpret_cast<const float4 *>(&prod[tid][4 * k4]);
+        sc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(sc, v.x), v.y), v.z), v.w);
+      }
       const int64_t i = s_i[tid];
       scores[base_r + i] = sc;
       const bool c = s_c[tid] != 0;
@@ -1155,6 +1181,7 @@ __global__ void __launch_bounds__(256, 3) score64_kernel(
       if (c && (finite || mode == 1)) insert_top(top, make_key((double)sc, sh.row_start + i));
     }
   }
+  cp_async_wait<0>();
   if (cnt) atomicAdd(&s_count, cnt);
   __syncthreads();  // prod fully consumed before the key lists reuse it
   block_merge_top(top, s_keys, block_keys + ((int64_t)b * gridDim.x + blockIdx.x) * kTopK,
@@ -1558,9 +1585,10 @@ int s2v_colsum_residual(s2v_dtype dt, const s2v_shard *sh, int K, const void *h,
 }
 
 int s2v_score_blocks(const s2v_shard *sh) {
-  // one resident wave (3 CTAs per SM) at most; rows are dealt round-robin
+  // one resident wave of score64_kernel (2 CTAs per SM) at most; rows are
+  // dealt round-robin
   int64_t n = (sh->num_rows + kScoreRowsPerBlock - 1) / kScoreRowsPerBlock;
-  if (n > kNumSMs * 3) n = kNumSMs * 3;
+  if (n > kNumSMs * 2) n = kNumSMs * 2;
   return (int)(n < 1 ? 1 : n);
 }
 
@@ -1576,7 +1604,9 @@ int s2v_score(s2v_dtype dt, const s2v_shard *sh, int K, const void *h, const voi
   size_t elem = dt == S2V_F32 ? 4 : 8;
   size_t smem = elem * ((size_t)K * (K + 1) + 16 * (size_t)K) + sizeof(Key) * 256 * kTopK;
   if (dt == S2V_F32 && K == 64) {
-    score64_kernel<<<grid, 256, 0, st>>>(*sh, (const float *)h, (const float *)u1,
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(score64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kScoreSmem));
+    score64_kernel<<<grid, 256, kScoreSmem, st>>>(*sh, (const float *)h, (const float *)u1,
                                          (const float *)theta6, (const float *)theta7,
                                          cand_override, mode, (float *)scores, (Key *)block_keys,
                                          counts);
@@ -1610,7 +1640,9 @@ int s2v_score_cached(const s2v_shard *sh, const float *h, const float *u1, const
   S2V_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(int64_t), st));
   const int nblk = s2v_score_blocks(sh);
   if (!rows) {  // every active row: scores, keys, and the cache
-    score64_kernel<<<dim3(nblk, 1), 256, 0, st>>>(*sh, h, u1, theta6, theta7, nullptr, mode,
+    S2V_CUDA_CHECK(cudaFuncSetAttribute(score64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kScoreSmem));
+    score64_kernel<<<dim3(nblk, 1), 256, kScoreSmem, st>>>(*sh, h, u1, theta6, theta7, nullptr, mode,
                                                   scores, (Key *)block_keys, counts, prod_cache, 1);
     S2V_LAUNCH_CHECK();
     return S2V_OK;
@@ -1620,7 +1652,9 @@ int s2v_score_cached(const s2v_shard *sh, const float *h, const float *u1, const
   fr.active_n = nrows;
   fr.active_ptr = nullptr;
   fr.active_cols = nullptr;
-  score64_kernel<<<dim3(nblk, 1), 256, 0, st>>>(fr, h, u1, theta6, theta7, nullptr, mode, scores,
+  S2V_CUDA_CHECK(cudaFuncSetAttribute(score64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kScoreSmem));
+  score64_kernel<<<dim3(nblk, 1), 256, kScoreSmem, st>>>(fr, h, u1, theta6, theta7, nullptr, mode, scores,
                                                 (Key *)block_keys, counts, prod_cache, 0);
   S2V_LAUNCH_CHECK();
   score_sum64_kernel<<<nblk, 256, 0, st>>>(*sh, u1, theta7, prod_cache, mode, (Key *)block_keys,
