@@ -153,9 +153,27 @@ __device__ __forceinline__ void gather_row64_g8(const int64_t e0, const int64_t 
   a0 = make_float4(0.f, 0.f, 0.f, 0.f);
   a1 = a0;
   const int cnt = (int)(e1 - e0);
+  auto col_of = [&](int e) {
+    return e + l8 < cnt ? ldg_u32_pol(cols + e0 + e + l8, pol_cold) : S2V_DEAD;
+  };
+  // TABLE: a neighbour's table row needs its id, then its degree -- two
+  // dependent trips to L2 before the (L1-resident) table rows.  Pipelined:
+  // the ids two groups ahead and the degrees one group ahead are in flight
+  // while this group's table rows are added.
+  uint32_t id_next = 0, col_next2 = 0;
+  if (TABLE) {
+    id_next = source_row<TABLE>(col_of(0), deg_of, sol_of);
+    col_next2 = col_of(8);
+  }
   for (int e8 = 0; e8 < cnt; e8 += 8) {
-    const uint32_t id = source_row<TABLE>(
-        e8 + l8 < cnt ? ldg_u32_pol(cols + e0 + e8 + l8, pol_cold) : S2V_DEAD, deg_of, sol_of);
+    uint32_t id;
+    if (TABLE) {
+      id = id_next;
+      id_next = source_row<TABLE>(col_next2, deg_of, sol_of);
+      col_next2 = col_of(e8 + 16);
+    } else {
+      id = source_row<TABLE>(col_of(e8), deg_of, sol_of);
+    }
     if (pf && l8 >= 4 && !(id & S2V_DEAD)) {  // rows 4..7 toward L2 while 0..3 load
       const float *src = h_in + (int64_t)id * 64;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
