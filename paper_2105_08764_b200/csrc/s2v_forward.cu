@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(256, 4) round64_kernel(
           TABLE ? 0u : (uint32_t)(r >= 0 ? (r / sh.num_rows) * sh.world * sh.rows_max : 0);
       float4 a0, a1;
       gather_row64_g8<TABLE>(e0, e1, cl, h_in, l8, qmask, qbase, hot_rows, pol_hot, pol_cold,
-                             deg_src, sol_of, hot_lo, a0, a1, !TABLE && pf);
+                             deg_src, sol_of, hot_lo, a0, a1, TABLE ? 0 : pf);
       *reinterpret_cast<float4 *>(&ms[lr][4 * l8]) = a0;
       *reinterpret_cast<float4 *>(&ms[lr][32 + 4 * l8]) = a1;
       if (m_out && r >= 0) {

@@ -149,7 +149,7 @@ __device__ __forceinline__ void gather_row64_g8(const int64_t e0, const int64_t 
                                                 const int32_t *__restrict__ deg_of,
                                                 const uint8_t *__restrict__ sol_of,
                                                 uint32_t hot_lo, float4 &a0, float4 &a1,
-                                                bool pf = false) {
+                                                int pf = 0) {
   a0 = make_float4(0.f, 0.f, 0.f, 0.f);
   a1 = a0;
   const int cnt = (int)(e1 - e0);
@@ -168,6 +168,7 @@ __device__ __forceinline__ void gather_row64_g8(const int64_t e0, const int64_t 
     col_next2 = col_of(8);
   } else {
     id_next = col_of(0);
+    if (pf & 2) col_next2 = col_of(8);
   }
   for (int e8 = 0; e8 < cnt; e8 += 8) {
     uint32_t id;
@@ -175,12 +176,24 @@ __device__ __forceinline__ void gather_row64_g8(const int64_t e0, const int64_t 
       id = id_next;
       id_next = source_row<TABLE>(col_next2, deg_of, sol_of);
       col_next2 = col_of(e8 + 16);
+    } else if (pf & 2) {  // ids two groups ahead: the next group's are here
+      id = source_row<TABLE>(id_next, deg_of, sol_of);
+      id_next = col_next2;
+      col_next2 = col_of(e8 + 16);
     } else {
       id = source_row<TABLE>(id_next, deg_of, sol_of);
       id_next = col_of(e8 + 8);
     }
-    if (pf && l8 >= 4 && !(id & S2V_DEAD)) {  // rows 4..7 toward L2 while 0..3 load
+    // pf bit 0: rows 4..7 toward L2 while 0..3 load (bit 2: first group
+    // only); bit 1: the next group's 8 rows toward L2 (its ids are already
+    // in id_next), so 16 rows per group are in flight without registers
+    if ((pf & 1) && (!(pf & 4) || e8 == 0) && l8 >= 4 && !(id & S2V_DEAD)) {
       const float *src = h_in + (int64_t)id * 64;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 32));
+    }
+    if (!TABLE && (pf & 2) && !(id_next & S2V_DEAD)) {
+      const float *src = h_in + (int64_t)id_next * 64;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 32));
     }
@@ -212,13 +225,17 @@ __device__ __forceinline__ void gather_row64_g8(const int64_t e0, const int64_t 
   }
 }
 
-// gather_row64_g8 prefetches rows 4..7 of each 8-id group into L2 while rows
-// 0..3 load (measured: round 2.306 -> 2.288 ms at cfg3, spmm_t 3.84 -> 3.76
-// ms per B = 2 launch); S2V_G8_PF=0 turns it off for A/B runs
+// gather_row64_g8's L2 prefetch mode (bits of pf): 1 = rows 4..7 of each
+// 8-id group while rows 0..3 load (round 2.306 -> 2.288 ms at cfg3, spmm_t
+// 3.84 -> 3.76 ms per B = 2 launch); 2 (default) = the next group's 8 rows,
+// ids two groups ahead (cfg3 step 9.30-9.34 -> 9.10-9.27 ms, two boxes;
+// prefetching two groups ahead measured 10.76 ms: the prefetched lines are
+// evicted before use); 4 = bit 0 on the first group only; 0 = off.
+// S2V_G8_PF overrides it for A/B runs
 inline int g8_prefetch() {
   static const int v = [] {
     const char *e = getenv("S2V_G8_PF");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
   return v;
 }
