@@ -71,9 +71,17 @@ __global__ void sol_bits_kernel(const uint8_t *__restrict__ sol_phys, int64_t n,
   }
 }
 
+// Rows with more than kInitLong entries (BA / R-MAT hubs: up to ~10^5) are
+// not walked by one 8-lane group, 32 entries per dependent trip to HBM (a
+// 9,400-entry BA(2M,16) hub alone took ~300 us, the whole kernel's time):
+// shard_init_kernel appends them to a list and shard_init_long_kernel gives
+// each one a CTA, 1,024 entries per trip.
+constexpr int64_t kInitLong = 1024;
+
 __global__ void shard_init_kernel(s2v_shard sh, const uint32_t *__restrict__ cols_src,
                                   const uint8_t *__restrict__ sol_phys,
-                                  const uint32_t *__restrict__ sol_bits) {
+                                  const uint32_t *__restrict__ sol_bits,
+                                  int64_t *__restrict__ long_rows, int *__restrict__ long_n) {
   const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
   const uint32_t *src = cols_src ? cols_src : sh.cols;
@@ -93,12 +101,17 @@ __global__ void shard_init_kernel(s2v_shard sh, const uint32_t *__restrict__ col
     }
     uint8_t s = 0;
     int cnt = 0;
+    bool mine = ok;
     if (ok) {
       s = sol_phys[(b * sh.world + sh.rank) * sh.rows_max + i];
-      const int64_t e1 = sh.row_ptr[r + 1];
+      const int64_t e0 = sh.row_ptr[r], e1 = sh.row_ptr[r + 1];
+      if (e1 - e0 > kInitLong) {  // shard_init_long_kernel's row
+        mine = false;
+        if (sub == 0) long_rows[atomicAdd(long_n, 1)] = r;
+      }
       // four 8-entry steps per iteration: a BA row's ~32 column loads, then
       // its bitmap lookups, all in flight together
-      for (int64_t e = sh.row_ptr[r] + sub; e < e1; e += 32) {
+      for (int64_t e = e0 + sub; mine && e < e1; e += 32) {
         uint32_t c[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) c[q] = e + 8 * q < e1 ? src[e + 8 * q] & ~S2V_DEAD : 0u;
@@ -113,7 +126,7 @@ __global__ void shard_init_kernel(s2v_shard sh, const uint32_t *__restrict__ col
     }
 #pragma unroll
     for (int o = 4; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (ok && sub == 0) {
+    if (mine && sub == 0) {
       sh.rdeg[r] = cnt;
       sh.sol[r] = s;
       sh.cand[r] = (cnt > 0 && !s) ? 1 : 0;
@@ -138,6 +151,53 @@ __global__ void shard_init_kernel(s2v_shard sh, const uint32_t *__restrict__ col
     }
   }
   if (lane == 0 && acc) atomicAdd((unsigned long long *)&sh.residual[acc_b], acc);
+}
+
+// One CTA per listed long row: entries tid + 256 j, four per thread in
+// flight, the same dead-bit rule and column copy as shard_init_kernel
+__global__ void __launch_bounds__(256) shard_init_long_kernel(
+    s2v_shard sh, const uint32_t *__restrict__ cols_src, const uint8_t *__restrict__ sol_phys,
+    const uint32_t *__restrict__ sol_bits, const int64_t *__restrict__ long_rows,
+    const int *__restrict__ long_n) {
+  __shared__ int s_cnt;
+  const uint32_t *src = cols_src ? cols_src : sh.cols;
+  const int n = *long_n;
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const int64_t r = long_rows[k];
+    int64_t b = 0, i = r;
+    if (sh.batch > 1) {
+      b = r / sh.num_rows;
+      i = r - b * sh.num_rows;
+    }
+    const uint8_t s = sol_phys[(b * sh.world + sh.rank) * sh.rows_max + i];
+    const int64_t e1 = sh.row_ptr[r + 1];
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    int cnt = 0;
+    for (int64_t e = sh.row_ptr[r] + threadIdx.x; e < e1; e += 4 * 256) {
+      uint32_t c[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) c[q] = e + 256 * q < e1 ? src[e + 256 * q] & ~S2V_DEAD : 0u;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        if (e + 256 * q >= e1) break;
+        const bool dead = s || ((__ldg(sol_bits + (c[q] >> 5)) >> (c[q] & 31)) & 1u);
+        sh.cols[e + 256 * q] = c[q] | (dead ? S2V_DEAD : 0u);
+        cnt += !dead;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_cnt, cnt);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sh.rdeg[r] = s_cnt;
+      sh.sol[r] = s;
+      sh.cand[r] = (s_cnt > 0 && !s) ? 1 : 0;
+      if (s_cnt) atomicAdd((unsigned long long *)&sh.residual[b], (unsigned long long)s_cnt);
+    }
+    __syncthreads();  // s_cnt is reset for the next row
+  }
 }
 
 // S of every physical row after a group apply: the applied picks (global
@@ -499,7 +559,11 @@ int s2v_shard_init(const s2v_shard *sh, const uint32_t *cols_src, const uint8_t 
   } scratch;
   int dev = 0;
   S2V_CUDA_CHECK(cudaGetDevice(&dev));
-  const size_t need = 4 * (size_t)((nphys + 31) / 32);
+  // sol bitmap, then the long-row list (at most nnz / kInitLong rows) and
+  // its count
+  const size_t bits_bytes = (4 * (size_t)((nphys + 31) / 32) + 7) & ~(size_t)7;
+  const size_t list_n = (size_t)(sh->nnz / kInitLong + 1);
+  const size_t need = bits_bytes + 8 * list_n + 8;
   if (scratch.dev != dev || scratch.bytes < need) {
     if (scratch.p && scratch.dev == dev) {
       S2V_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -511,13 +575,22 @@ int s2v_shard_init(const s2v_shard *sh, const uint32_t *cols_src, const uint8_t 
     scratch.bytes = need;
   }
   uint32_t *bits = scratch.p;
+  int64_t *long_rows = reinterpret_cast<int64_t *>(reinterpret_cast<char *>(scratch.p) + bits_bytes);
+  int *long_n = reinterpret_cast<int *>(long_rows + list_n);
+  S2V_CUDA_CHECK(cudaMemsetAsync(long_n, 0, sizeof(int), st));
   sol_bits_kernel<<<(unsigned)std::min<int64_t>(((nphys + 31) / 32 + 255) / 256, kNumSMs * 8),
                     256, 0, st>>>(sol_phys, nphys, bits);
   S2V_LAUNCH_CHECK();
   int64_t blocks = (rows * 8 + 255) / 256;
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
-  shard_init_kernel<<<(unsigned)blocks, 256, 0, st>>>(*sh, cols_src, sol_phys, bits);
+  shard_init_kernel<<<(unsigned)blocks, 256, 0, st>>>(*sh, cols_src, sol_phys, bits, long_rows,
+                                                       long_n);
   S2V_LAUNCH_CHECK();
+  if (sh->nnz > kInitLong) {
+    shard_init_long_kernel<<<(unsigned)std::min<int64_t>(sh->nnz / kInitLong, kNumSMs * 4), 256,
+                             0, st>>>(*sh, cols_src, sol_phys, bits, long_rows, long_n);
+    S2V_LAUNCH_CHECK();
+  }
   return S2V_OK;
 }
 

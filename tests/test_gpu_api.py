@@ -184,6 +184,43 @@ class TestStateTransitions:
             assert np.array_equal(ra, rb)
 
 
+@pytest.mark.parametrize("p", [1, 2])
+def test_state_build_with_long_rows(p):
+    """Rows over 1,024 entries take shard_init's CTA-per-row pass: candidates,
+    residual entries and per-slot residual counts equal the state.py:60-90
+    definition (an entry is alive iff neither endpoint is in S) on hubs of
+    3,000 and 1,500 entries in a batch of two solutions, at P = 1 and 2."""
+    rng = np.random.default_rng(3)
+    n = 4000
+    edges = {(0, v) for v in range(1, 3001)} | {(1, v) for v in range(2000, 3500)}
+    while len(edges) < 3000 + 1500 + 6000:
+        a, b = sorted(rng.integers(2, n, 2).tolist())
+        if a != b:
+            edges.add((a, b))
+    g = P.Graph(n, sorted(edges))
+    sol = (rng.random((2, n)) < 0.05).astype(np.uint8)
+    sol[1, 1] = 1  # the second hub in S in slot 1
+    E = np.array(sorted(edges))
+
+    def worker(comm):
+        part = P.partition_rows(n, comm.size)[comm.rank]
+        st = P.PartitionedState([g, g], part, solutions=sol)
+        out = []
+        for b in range(2):
+            cand = comm.all_gather(st.cand[b], axis=-1)
+            rows, cols = st.local_residual_coo(b)
+            out.append((cand, set(zip(rows.tolist(), cols.tolist())), st.local_residual[b]))
+        return out
+    res = P.run_workers(p, worker)
+    for b in range(2):
+        alive = E[(sol[b, E[:, 0]] == 0) & (sol[b, E[:, 1]] == 0)]
+        want = {(int(u), int(v)) for u, v in alive} | {(int(v), int(u)) for u, v in alive}
+        deg = np.bincount(alive.ravel(), minlength=n)
+        assert np.array_equal(res[0][b][0], ((deg > 0) & (sol[b] == 0)).astype(np.uint8))
+        assert set().union(*(r[b][1] for r in res)) == want
+        assert sum(int(r[b][2]) for r in res) == 2 * len(alive)
+
+
 class TestActAndTargets:
     """pkg/tests/test_agent.py:46-112."""
 
