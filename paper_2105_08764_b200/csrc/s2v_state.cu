@@ -78,10 +78,43 @@ __global__ void sol_bits_kernel(const uint8_t *__restrict__ sol_phys, int64_t n,
 // each one a CTA, 1,024 entries per trip.
 constexpr int64_t kInitLong = 1024;
 
+// Coarse S summary for shard_init_kernel's neighbour test: bit t of word j
+// is set iff a node of [(32 j + t) << lg, +2^lg) is in S (lg >= 3, 32 KB for
+// up to 2^(18 + lg) physical rows).  It lives in shared memory, where 32
+// random lookups cost a few bank wavefronts instead of up to 32 L1 lines,
+// and only a set summary bit sends the test to the exact bitmap -- the 64M
+// random bitmap lookups of BA(2M,16) were the kernel's L1-bound time.
+constexpr int kSumWords = 8192;
+
+__global__ void sol_summary_kernel(const uint32_t *__restrict__ bits, int64_t n, int lg,
+                                   uint32_t *__restrict__ summary) {
+  const int64_t nwords = (n + 31) / 32;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < kSumWords;
+       j += gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    for (int t = 0; t < 32; t++) {
+      const int64_t lo = ((int64_t)(32 * j + t)) << lg, hi = lo + ((int64_t)1 << lg);
+      bool any = false;
+      for (int64_t w = lo >> 5; w < nwords && (w << 5) < hi && !any; w++) {
+        uint32_t m = bits[w];
+        if (lg < 5) m = (m >> (lo & 31)) & ((1u << (1 << lg)) - 1u);
+        any = m != 0;
+      }
+      v |= (any ? 1u : 0u) << t;
+    }
+    summary[j] = v;
+  }
+}
+
 __global__ void shard_init_kernel(s2v_shard sh, const uint32_t *__restrict__ cols_src,
                                   const uint8_t *__restrict__ sol_phys,
                                   const uint32_t *__restrict__ sol_bits,
-                                  int64_t *__restrict__ long_rows, int *__restrict__ long_n) {
+                                  int64_t *__restrict__ long_rows, int *__restrict__ long_n,
+                                  const uint32_t *__restrict__ summary, int lg) {
+  extern __shared__ uint32_t s_sum[];  // [kSumWords]
+  for (int j = threadIdx.x; j < kSumWords / 4; j += blockDim.x)
+    reinterpret_cast<uint4 *>(s_sum)[j] = reinterpret_cast<const uint4 *>(summary)[j];
+  __syncthreads();
   const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
   const uint32_t *src = cols_src ? cols_src : sh.cols;
@@ -90,21 +123,37 @@ __global__ void shard_init_kernel(s2v_shard sh, const uint32_t *__restrict__ col
   int64_t acc_b = -1;
   unsigned long long acc = 0;
   const int64_t wstride = ((gridDim.x * (int64_t)blockDim.x) >> 5) * 4;
-  for (int64_t w0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 4; w0 < nrows;
-       w0 += wstride) {  // warp-uniform loop: rows w0 + grp
+  // the next iteration's row range and S byte are loaded one iteration
+  // ahead, so each row costs one dependent trip to HBM (its columns)
+  auto row_info = [&](int64_t r, int64_t &e0, int64_t &e1, uint8_t &s) {
+    e0 = e1 = 0;
+    s = 0;
+    if (r < nrows) {
+      int64_t b = 0, i = r;
+      if (sh.batch > 1) {
+        b = r / sh.num_rows;
+        i = r - b * sh.num_rows;
+      }
+      s = sol_phys[(b * sh.world + sh.rank) * sh.rows_max + i];
+      e0 = sh.row_ptr[r];
+      e1 = sh.row_ptr[r + 1];
+    }
+  };
+  int64_t w0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 4;
+  int64_t n_e0, n_e1;
+  uint8_t n_s;
+  row_info(w0 + grp, n_e0, n_e1, n_s);
+  for (; w0 < nrows; w0 += wstride) {  // warp-uniform loop: rows w0 + grp
     const int64_t r = w0 + grp;
     const bool ok = r < nrows;
-    int64_t b = 0, i = r;
-    if (ok && sh.batch > 1) {
-      b = r / sh.num_rows;
-      i = r - b * sh.num_rows;
-    }
-    uint8_t s = 0;
+    int64_t b = 0;
+    if (ok && sh.batch > 1) b = r / sh.num_rows;
+    const int64_t e0 = n_e0, e1 = n_e1;
+    const uint8_t s = n_s;
+    row_info(r + wstride, n_e0, n_e1, n_s);
     int cnt = 0;
     bool mine = ok;
     if (ok) {
-      s = sol_phys[(b * sh.world + sh.rank) * sh.rows_max + i];
-      const int64_t e0 = sh.row_ptr[r], e1 = sh.row_ptr[r + 1];
       if (e1 - e0 > kInitLong) {  // shard_init_long_kernel's row
         mine = false;
         if (sub == 0) long_rows[atomicAdd(long_n, 1)] = r;
@@ -118,7 +167,9 @@ __global__ void shard_init_kernel(s2v_shard sh, const uint32_t *__restrict__ col
 #pragma unroll
         for (int q = 0; q < 4; q++) {
           if (e + 8 * q >= e1) break;
-          const bool dead = s || ((__ldg(sol_bits + (c[q] >> 5)) >> (c[q] & 31)) & 1u);
+          const uint32_t cs = c[q] >> lg;
+          const bool dead = s || (((s_sum[cs >> 5] >> (cs & 31)) & 1u) &&
+                                  ((__ldg(sol_bits + (c[q] >> 5)) >> (c[q] & 31)) & 1u));
           sh.cols[e + 8 * q] = c[q] | (dead ? S2V_DEAD : 0u);
           cnt += !dead;
         }
@@ -563,7 +614,7 @@ int s2v_shard_init(const s2v_shard *sh, const uint32_t *cols_src, const uint8_t 
   // its count
   const size_t bits_bytes = (4 * (size_t)((nphys + 31) / 32) + 7) & ~(size_t)7;
   const size_t list_n = (size_t)(sh->nnz / kInitLong + 1);
-  const size_t need = bits_bytes + 8 * list_n + 8;
+  const size_t need = bits_bytes + 8 * list_n + 8 + 16 + 4 * kSumWords;
   if (scratch.dev != dev || scratch.bytes < need) {
     if (scratch.p && scratch.dev == dev) {
       S2V_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -577,14 +628,28 @@ int s2v_shard_init(const s2v_shard *sh, const uint32_t *cols_src, const uint8_t 
   uint32_t *bits = scratch.p;
   int64_t *long_rows = reinterpret_cast<int64_t *>(reinterpret_cast<char *>(scratch.p) + bits_bytes);
   int *long_n = reinterpret_cast<int *>(long_rows + list_n);
+  uint32_t *summary = reinterpret_cast<uint32_t *>(
+      (reinterpret_cast<uintptr_t>(long_n + 2) + 15) & ~(uintptr_t)15);  // uint4 loads
+  int lg = 3;
+  while (((int64_t)kSumWords * 32 << lg) < nphys) lg++;
   S2V_CUDA_CHECK(cudaMemsetAsync(long_n, 0, sizeof(int), st));
   sol_bits_kernel<<<(unsigned)std::min<int64_t>(((nphys + 31) / 32 + 255) / 256, kNumSMs * 8),
                     256, 0, st>>>(sol_phys, nphys, bits);
   S2V_LAUNCH_CHECK();
+  sol_summary_kernel<<<kSumWords / 256, 256, 0, st>>>(bits, nphys, lg, summary);
+  S2V_LAUNCH_CHECK();
+  // one resident wave (the loop is grid-strided and pipelined per warp)
+  static const int per_sm = [] {
+    int n = 0;
+    cudaFuncSetAttribute(shard_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         4 * kSumWords);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, shard_init_kernel, 256, 4 * kSumWords);
+    return n > 0 ? n : 4;
+  }();
   int64_t blocks = (rows * 8 + 255) / 256;
-  if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
-  shard_init_kernel<<<(unsigned)blocks, 256, 0, st>>>(*sh, cols_src, sol_phys, bits, long_rows,
-                                                       long_n);
+  if (blocks > (int64_t)kNumSMs * per_sm) blocks = (int64_t)kNumSMs * per_sm;
+  shard_init_kernel<<<(unsigned)blocks, 256, 4 * kSumWords, st>>>(
+      *sh, cols_src, sol_phys, bits, long_rows, long_n, summary, lg);
   S2V_LAUNCH_CHECK();
   if (sh->nnz > kInitLong) {
     shard_init_long_kernel<<<(unsigned)std::min<int64_t>(sh->nnz / kInitLong, kNumSMs * 4), 256,
