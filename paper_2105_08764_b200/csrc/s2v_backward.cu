@@ -1089,16 +1089,29 @@ __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
       for (int a = 0; a < 4; a++)
 #pragma unroll
         for (int c = 0; c < 4; c++) acc[a][c] = 0.f;
-#pragma unroll 4
-      for (int k = 0; k < 64; k++) {
-        const float4 t = f4(&th3[k][4 * lo]);
+      // dz rows read as float4 along k (4 k per load: 8 shared loads per 64
+      // FMA instead of 5 per 16); each output stays the chain k = 0..63
+#pragma unroll 2
+      for (int k0 = 0; k0 < 64; k0 += 4) {
+        float dv[4][4];
 #pragma unroll
         for (int a = 0; a < 4; a++) {
-          const float d = dzs[4 * hi + a][k];
-          acc[a][0] = __fmaf_rn(t.x, d, acc[a][0]);
-          acc[a][1] = __fmaf_rn(t.y, d, acc[a][1]);
-          acc[a][2] = __fmaf_rn(t.z, d, acc[a][2]);
-          acc[a][3] = __fmaf_rn(t.w, d, acc[a][3]);
+          const float4 d4 = f4(&dzs[4 * hi + a][k0]);
+          dv[a][0] = d4.x;
+          dv[a][1] = d4.y;
+          dv[a][2] = d4.z;
+          dv[a][3] = d4.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const float4 t = f4(&th3[k0 + i][4 * lo]);
+#pragma unroll
+          for (int a = 0; a < 4; a++) {
+            acc[a][0] = __fmaf_rn(t.x, dv[a][i], acc[a][0]);
+            acc[a][1] = __fmaf_rn(t.y, dv[a][i], acc[a][1]);
+            acc[a][2] = __fmaf_rn(t.z, dv[a][i], acc[a][2]);
+            acc[a][3] = __fmaf_rn(t.w, dv[a][i], acc[a][3]);
+          }
         }
       }
 #pragma unroll
@@ -1122,9 +1135,13 @@ __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
         }
       }
     }
-    // dtheta1[k] += dz[row][k] sol[row]
-    if (tid < 64)
-      for (int row = 0; row < kT64; row++) p1 = __fmaf_rn(dzs[row][tid], s_sol[row], p1);
+    // dtheta1[k] += dz[row][k] sol[row]: every thread, rows g (mod 4) of
+    // column k (tid = 64 g + k), four partials summed in g order at the end
+    // (one warp pair walking all rows serially held the other six warps at
+    // the next barrier)
+#pragma unroll 4
+    for (int row = tid >> 6; row < kT64; row += 4)
+      p1 = __fmaf_rn(dzs[row][tid & 63], s_sol[row], p1);
   }
   __syncthreads();
   // reduce p2 over the 16 row groups (hi), then write the partial row
@@ -1132,10 +1149,14 @@ __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
   for (int c = 0; c < 4; c++) red[hi][4 * lo + c] = p2[c];
   __syncthreads();
   float *out = partial + (int64_t)blockIdx.x * (2 * 64 + 4096);
-  if (tid < 64) {
-    float s2 = 0.f;
+  float s2 = 0.f;
+  if (tid < 64)
     for (int q = 0; q < 16; q++) s2 += red[q][tid];
-    out[tid] = p1;
+  __syncthreads();
+  red[tid >> 6][tid & 63] = p1;
+  __syncthreads();
+  if (tid < 64) {
+    out[tid] = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
     out[64 + tid] = s2;
   }
 #pragma unroll
