@@ -668,14 +668,14 @@ def main():
     achieved = algo_bytes / (round_ms * 1e-3) / 1e9
     traffic = None
     try:  # DRAM bytes per launch from the committed ncu --set full capture
-        tr = json.loads((ROOT / "profiles" / "r2_round64_traffic.json").read_text())
+        tr = json.loads((ROOT / "profiles" / "r2s3_round64_traffic.json").read_text())
         if args.nodes == 2_000_000 and args.m == 16 and world == 1:
             traffic = tr["dram_bytes_per_launch"]
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "traffic_source": "profiles/r2_round64_traffic.json (ncu dram__bytes_read+write)",
+                "traffic_source": "profiles/r2s3_round64_traffic.json (ncu dram__bytes_read+write)",
                 "kernel": "round64_kernel (fused gather-SpMM + theta4 FMA chain + e12 + relu), "
                           "rounds 3..5 (round 2 gathers the per-degree h1 table, round 1 is "
                           "skipped)",
