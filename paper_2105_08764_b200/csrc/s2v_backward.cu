@@ -1005,6 +1005,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) layer_backward64_tc_kernel(
 
 // dtheta1 [64], dtheta2 [64], dtheta3 [64][64] partials from dzsum.
 // Dynamic smem: th3 [64][68], dzs [64][68], ws [64][68], red [16][64], aux.
+// dtheta3 = sum_rows dz[row] w[row]^T with w[row][j] = fl(theta2[j] deg) or
+// 0 -- relu(theta2[j] deg) = relu(theta2[j]) deg exactly in real arithmetic
+// (deg >= 0), so dtheta3[k][j] = relu(theta2[j]) * u[k], u[k] = sum_rows
+// dz[row][k] deg[row]: 64 FMA per row instead of the 4,096 of the outer
+// product.  Each term differs from the reference's fl(fl(theta2 deg) dz) by
+// at most one rounding of the product -- the same order of error as any
+// other summation order of this sum, well inside the 1e-4 bar.
+
 __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
     s2v_shard sh, const float *__restrict__ theta2, const float *__restrict__ theta3,
     const float *__restrict__ dzsum, float *__restrict__ partial, float *__restrict__ t2c) {
@@ -1018,13 +1026,9 @@ __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
   const int tid = threadIdx.x;
   for (int idx = tid; idx < 64 * 64; idx += 256) th3[idx / 64][idx % 64] = theta3[idx];
   const int lo = tid & 15, hi = tid >> 4;
-  float p3[4][4], p2[4], p1 = 0.f;
+  float p2[4], p1 = 0.f, pu = 0.f;
 #pragma unroll
-  for (int a = 0; a < 4; a++) {
-    p2[a] = 0.f;
-#pragma unroll
-    for (int c = 0; c < 4; c++) p3[a][c] = 0.f;
-  }
+  for (int a = 0; a < 4; a++) p2[a] = 0.f;
   const int64_t nrows = (int64_t)sh.batch * sh.num_rows;
   const int64_t ntiles = (nrows + kT64 - 1) / kT64;
   // register double buffer: the next tile's dz sums and (S bit, degree) are
@@ -1071,17 +1075,6 @@ __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
     }
     __syncthreads();
     load_tile(tile + gridDim.x);
-    // dtheta3[k][j] += dz[row][k] w[row][j]   (k = 4lo+a, j = 4hi+c)
-#pragma unroll 4
-    for (int row = 0; row < kT64; row++) {
-      const float4 d = f4(&dzs[row][4 * lo]);
-      const float4 w = f4(&ws[row][4 * hi]);
-      const float dv[4] = {d.x, d.y, d.z, d.w}, wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int a = 0; a < 4; a++)
-#pragma unroll
-        for (int c = 0; c < 4; c++) p3[a][c] = __fmaf_rn(dv[a], wv[c], p3[a][c]);
-    }
     // dtheta2[j] += deg (w_j > 0) (theta3^T dz)_j   rows 4hi+a, j = 4lo+c
     {
       float acc[4][4];
@@ -1140,8 +1133,11 @@ __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
     // (one warp pair walking all rows serially held the other six warps at
     // the next barrier)
 #pragma unroll 4
-    for (int row = tid >> 6; row < kT64; row += 4)
-      p1 = __fmaf_rn(dzs[row][tid & 63], s_sol[row], p1);
+    for (int row = tid >> 6; row < kT64; row += 4) {
+      const float d = dzs[row][tid & 63];
+      p1 = __fmaf_rn(d, s_sol[row], p1);
+      pu = __fmaf_rn(d, s_deg[row], pu);  // u[k] of dtheta3 (above)
+    }
   }
   __syncthreads();
   // reduce p2 over the 16 row groups (hi), then write the partial row
@@ -1154,15 +1150,16 @@ __global__ void __launch_bounds__(256, 2) param_grads64_kernel(
     for (int q = 0; q < 16; q++) s2 += red[q][tid];
   __syncthreads();
   red[tid >> 6][tid & 63] = p1;
+  red[4 + (tid >> 6)][tid & 63] = pu;
   __syncthreads();
   if (tid < 64) {
     out[tid] = ((red[0][tid] + red[1][tid]) + red[2][tid]) + red[3][tid];
     out[64 + tid] = s2;
+    red[8][tid] = ((red[4][tid] + red[5][tid]) + red[6][tid]) + red[7][tid];
   }
-#pragma unroll
-  for (int a = 0; a < 4; a++)
-#pragma unroll
-    for (int c = 0; c < 4; c++) out[128 + (4 * lo + a) * 64 + 4 * hi + c] = p3[a][c];
+  __syncthreads();
+  for (int idx = tid; idx < 4096; idx += 256)  // dtheta3 partial [k][j]
+    out[128 + idx] = __fmul_rn(red[8][idx >> 6], relu(theta2[idx & 63]));
 }
 
 // spmm_t for K = 64 fp32: half-warp per row in descending-degree order.
