@@ -337,8 +337,18 @@ template <class T>
 __global__ void reduce_partials_kernel(const T *__restrict__ partials, int nparts, int len,
                                        double *__restrict__ out) {
   for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < len; o += gridDim.x * blockDim.x) {
+    // same sequential order; 16 loads in flight ahead of the dependent adds
+    // (one L2 trip per part made a B = 32 reduce 32 us)
     double s = 0.0;
-    for (int p = 0; p < nparts; p++) s += (double)partials[(int64_t)p * len + o];
+    int p = 0;
+    for (; p + 16 <= nparts; p += 16) {
+      T v[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) v[q] = partials[(int64_t)(p + q) * len + o];
+#pragma unroll
+      for (int q = 0; q < 16; q++) s += (double)v[q];
+    }
+    for (; p < nparts; p++) s += (double)partials[(int64_t)p * len + o];
     out[o] = s;
   }
 }
