@@ -221,6 +221,31 @@ def test_state_build_with_long_rows(p):
         assert sum(int(r[b][2]) for r in res) == 2 * len(alive)
 
 
+def test_state_build_coarse_summary_many_nodes():
+    """9M nodes: shard_init's shared-memory S summary covers 2^6 nodes per bit
+    (the multi-word summary path); candidates and the residual count still
+    equal the definition, with a 2,000-entry hub and a 1% solution."""
+    rng = np.random.default_rng(11)
+    n = 9_000_000
+    a = rng.integers(0, n, 60_000)
+    b = rng.integers(0, n, 60_000)
+    keep = a != b
+    pairs = np.unique(np.sort(np.stack([a[keep], b[keep]], 1), axis=1), axis=0)
+    hub = np.stack([np.zeros(2000, np.int64), rng.choice(np.arange(1, n), 2000, replace=False)], 1)
+    E = np.unique(np.concatenate([pairs, hub]), axis=0)
+    g = P.Graph(n, [tuple(e) for e in E.tolist()])
+    sol = (rng.random((1, n)) < 0.01).astype(np.uint8)
+
+    def worker(comm):
+        st = P.PartitionedState([g], P.partition_rows(n, 1)[0], solutions=sol)
+        return st.cand[0].copy(), int(st.local_residual[0])
+    cand, resid = P.run_workers(1, worker)[0]
+    alive = E[(sol[0, E[:, 0]] == 0) & (sol[0, E[:, 1]] == 0)]
+    deg = np.bincount(alive.ravel(), minlength=n)
+    assert np.array_equal(cand, ((deg > 0) & (sol[0] == 0)).astype(np.uint8))
+    assert resid == 2 * len(alive)
+
+
 class TestActAndTargets:
     """pkg/tests/test_agent.py:46-112."""
 
